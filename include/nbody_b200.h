@@ -1,0 +1,189 @@
+/*
+ * nbody_b200.h -- C ABI of libnbody_b200.so, the B200 (sm_100a) all-pairs
+ * N-body hot path that sits behind the reference package's N-body entry point
+ * (arXiv 2203.08263 artifact `nbodybench`).  Paths in citations are relative to
+ * /root/reference/pkg/src/nbodybench/.
+ *
+ * Two families of entry points:
+ *
+ *  1. nb_host_*  -- HOST pointers, synchronous.  These are exactly the calls the
+ *     reference's own FFI for this path makes into its compiled kernel module
+ *     (Cython `_accel_cy`, bound through typed memoryviews), with the same
+ *     argument order and meaning, plus the body count that a memoryview carries
+ *     implicitly.  `block` and `threads` are accepted and ignored: the GPU uses
+ *     its own tiling and all SMs.  `recip` selects the algebraic form on the CPU;
+ *     the GPU always evaluates m*d*rsqrt(d2)^3, which the reference pins as
+ *     equivalent to both forms (pkg/tests/test_kernels.py:220-227).
+ *
+ *  2. nb_dev_*   -- DEVICE pointers owned by the caller (e.g. torch tensors),
+ *     stream-ordered, asynchronous.  These carry the packed HBM layout the
+ *     kernels use and the i-shard / j-range arguments multi-GPU sharding needs.
+ *
+ * Packed layout (device): bodies are 4-vectors of the system precision,
+ *   pos4[k] = (x, y, z, m),  vel4[k] = (vx, vy, vz, 0),  acc4[k] = (ax, ay, az, 0)
+ * i.e. float4 (16 B) for *_f32 and double4 (32 B) for *_f64, 16 B aligned.
+ *
+ * Errors: every int-returning call returns 0 on success, else a nonzero code
+ * (NB_ERR_* below, or a cudaError_t value + 1000); nb_last_error() describes
+ * the last failure on the calling thread.  Argument errors are detected before
+ * any device work.  Non-finite results are NOT checked (kernels/__init__.py:190-191).
+ */
+#ifndef NBODY_B200_H_
+#define NBODY_B200_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define NB_OK 0
+#define NB_ERR_ARG 1       /* invalid argument (sizes, null pointers, modes)      */
+#define NB_ERR_WORKSPACE 2 /* workspace pointer null or smaller than required     */
+#define NB_ERR_NODEV 3     /* no CUDA device / not an sm_100 device               */
+#define NB_ERR_CUDA 1000   /* + cudaError_t                                       */
+
+/* Update modes of the fused force+integrate step (nb_dev_step_*).
+ * The velocity-Verlet loop of kernels.simulate (kernels/__init__.py:240-252) is
+ *   A(p); [kick if step>0]; kick-drift; ... ; A(p); kick
+ * and maps to NB_STEP_FIRST, NB_STEP_KICK_DRIFT x (steps-1), NB_STEP_FINAL_KICK.  */
+#define NB_MODE_ACCEL 0      /* a only: acc4 <- G*sum                               */
+#define NB_STEP_FIRST 1      /* step 0: dv=a*dt; p'=p+(v+half*dv)*dt; v+=dv; acc4<-a */
+#define NB_STEP_KICK_DRIFT 2 /* step>0: v+=(a-acc4)*f, f=real(0.5*dt); then FIRST    */
+#define NB_STEP_FINAL_KICK 3 /* after the loop: v+=(a-acc4)*f; acc4<-a; p unchanged */
+
+/* ---------------------------------------------------------------- host (FFI mirror) */
+
+/* Replaces _accel_cy.accel_soa (_accel_cy.pyx:114-152), called from
+ * kernels.compute_accelerations (kernels/__init__.py:199-202). */
+int nb_host_accel_soa_f32(const float* px, const float* py, const float* pz, const float* m,
+                          int64_t n, double g, double eps2, int recip, int64_t block,
+                          int threads, float* ax, float* ay, float* az);
+int nb_host_accel_soa_f64(const double* px, const double* py, const double* pz,
+                          const double* m, int64_t n, double g, double eps2, int recip,
+                          int64_t block, int threads, double* ax, double* ay, double* az);
+
+/* Replaces _accel_cy.accel_aos (_accel_cy.pyx:155-202): pos is C-contiguous (n,3). */
+int nb_host_accel_aos_f32(const float* pos, const float* m, int64_t n, double g, double eps2,
+                          float* ax, float* ay, float* az);
+int nb_host_accel_aos_f64(const double* pos, const double* m, int64_t n, double g,
+                          double eps2, double* ax, double* ay, double* az);
+
+/* Replaces _accel_cy.step_soa (_accel_cy.pyx:205-237), in place. */
+int nb_host_step_soa_f32(float* px, float* py, float* pz, float* vx, float* vy, float* vz,
+                         const float* ax, const float* ay, const float* az, int64_t n,
+                         double dt, int threads);
+int nb_host_step_soa_f64(double* px, double* py, double* pz, double* vx, double* vy,
+                         double* vz, const double* ax, const double* ay, const double* az,
+                         int64_t n, double dt, int threads);
+
+/* Replaces _accel_cy.step_aos (_accel_cy.pyx:240-259), in place on (n,3) arrays. */
+int nb_host_step_aos_f32(float* pos, float* vel, const float* ax, const float* ay,
+                         const float* az, int64_t n, double dt);
+int nb_host_step_aos_f64(double* pos, double* vel, const double* ax, const double* ay,
+                         const double* az, int64_t n, double dt);
+
+/* Replaces the whole of kernels.simulate (kernels/__init__.py:230-253) for an SoA
+ * system: runs `steps` velocity-Verlet steps (steps+1 force evaluations) on the
+ * device and writes the final state back IN PLACE into px..vz (the caller passes
+ * copies, as simulate's `state = sys_.copy()` does at :240). */
+int nb_host_simulate_soa_f32(float* px, float* py, float* pz, float* vx, float* vy, float* vz,
+                             const float* m, int64_t n, double g, double dt, double eps2,
+                             int64_t steps);
+int nb_host_simulate_soa_f64(double* px, double* py, double* pz, double* vx, double* vy,
+                             double* vz, const double* m, int64_t n, double g, double dt,
+                             double eps2, int64_t steps);
+
+/* ---------------------------------------------------------------- device (packed) */
+
+/* Workspace bytes a nb_dev_accel_* / nb_dev_step_* call needs for an i-shard of
+ * n_i bodies; precision_bytes is 4 or 8.  The workspace must be zero-filled once
+ * when first allocated and is left zeroed by every call (reusable). */
+int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i);
+
+/* Fused softened all-pairs force (+ optional velocity-Verlet update) for the
+ * target rows [i_begin, i_begin+n_i) of pos4 (n_all bodies) against the source
+ * bodies j in [j_begin, j_begin+j_count) taken modulo n_all (circular, so a
+ * shard can take "everything after my slice" as one range).
+ *
+ *   a_i = G * sum_j m_j (p_j - p_i) / (|p_j - p_i|^2 + eps2)^(3/2)
+ *
+ * mode         NB_MODE_ACCEL or one of NB_STEP_* (see above).
+ * exclude_self 1: skip j == i explicitly (required when eps2 == 0, where the
+ *              self pair is 0*inf); 0: self pair included, which adds exactly 0
+ *              when (real)eps2 > 0 and max_m * eps2^-1.5 is finite.
+ * carry        optional FP64 3*n_i buffer (SoA: x then y then z) of partial sums
+ *              (without G):
+ *              carry_mode 0: unused; 1: write the partial sums here and do not
+ *              finalize (first phase of a split j range); 2: add carry before
+ *              finalizing (second phase).
+ * acc4         n_i entries: a_prev in (kick modes), a out.
+ * vel4         n_i entries (step modes): updated in place.
+ * pos4_next    n_all entries (STEP_FIRST / STEP_KICK_DRIFT): rows
+ *              [i_begin, i_begin+n_i) receive the drifted (x,y,z,m).  Must not
+ *              alias pos4.
+ * stream       a cudaStream_t (NULL = legacy default stream). */
+int nb_dev_step_f32(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i,
+                    int64_t j_begin, int64_t j_count, double g, double eps2, double dt,
+                    int mode, int exclude_self, double* carry, int carry_mode, void* acc4,
+                    void* vel4, void* pos4_next, void* workspace, int64_t workspace_bytes,
+                    void* stream);
+int nb_dev_step_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i,
+                    int64_t j_begin, int64_t j_count, double g, double eps2, double dt,
+                    int mode, int exclude_self, double* carry, int carry_mode, void* acc4,
+                    void* vel4, void* pos4_next, void* workspace, int64_t workspace_bytes,
+                    void* stream);
+
+/* Device-resident kernels.simulate for one GPU: `steps` fused steps plus the final
+ * evaluation and kick (steps+1 launches), ping-ponging pos4_a <-> pos4_b.  On
+ * return (stream-ordered) the final positions are in pos4_a if steps is even,
+ * else in pos4_b; *final_in_b reports which (may be NULL). */
+int nb_dev_simulate_f32(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n,
+                        double g, double dt, double eps2, int64_t steps, int exclude_self,
+                        void* workspace, int64_t workspace_bytes, void* stream,
+                        int* final_in_b);
+int nb_dev_simulate_f64(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n,
+                        double g, double dt, double eps2, int64_t steps, int exclude_self,
+                        void* workspace, int64_t workspace_bytes, void* stream,
+                        int* final_in_b);
+
+/* Stand-alone update kernels on packed arrays (n entries each): the kick-drift
+ * of step_soa (_accel_cy.pyx:205-237) in place, and the trapezoidal kick of
+ * _kick (kernels/__init__.py:220-227): v += (a_new - a_old) * real(factor). */
+int nb_dev_drift_f32(void* pos4, void* vel4, const void* acc4, int64_t n, double dt,
+                     void* stream);
+int nb_dev_drift_f64(void* pos4, void* vel4, const void* acc4, int64_t n, double dt,
+                     void* stream);
+int nb_dev_kick_f32(void* vel4, const void* acc4_new, const void* acc4_old, int64_t n,
+                    double factor, void* stream);
+int nb_dev_kick_f64(void* vel4, const void* acc4_new, const void* acc4_old, int64_t n,
+                    double factor, void* stream);
+
+/* Softened potential energy  -G * sum_{i<j} m_i m_j / sqrt(|p_i-p_j|^2 + eps2)
+ * and kinetic energy / momentum of the packed state (validation.py:134-145),
+ * accumulated in FP64.  out6 (device, 6 doubles) <- (KE, PE, Px, Py, Pz, KE+PE).
+ * workspace: device scratch of at least 8*n bytes (per-body potentials). */
+int nb_dev_energy_f32(const void* pos4, const void* vel4, int64_t n, double g, double eps2,
+                      double* out6, void* workspace, int64_t workspace_bytes, void* stream);
+int nb_dev_energy_f64(const void* pos4, const void* vel4, int64_t n, double g, double eps2,
+                      double* out6, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- misc */
+
+const char* nb_last_error(void);
+const char* nb_version(void);
+/* Number of kernel launches this library has issued on the calling process. */
+int64_t nb_launch_count(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NBODY_B200_H_ */

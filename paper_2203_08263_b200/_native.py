@@ -1,0 +1,100 @@
+"""ctypes binding of libnbody_b200.so (the C ABI in include/nbody_b200.h).
+
+There is no fallback: if the shared library is missing or fails to load, every
+entry point raises.  Build it with ``python -m paper_2203_08263_b200._build``
+(or ``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from typing import Optional
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libnbody_b200.so")
+HEADER = os.path.join(os.path.dirname(_PKG), "include", "nbody_b200.h")
+
+NB_MODE_ACCEL = 0
+NB_STEP_FIRST = 1
+NB_STEP_KICK_DRIFT = 2
+NB_STEP_FINAL_KICK = 3
+
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_d = ctypes.c_double
+_i = ctypes.c_int
+
+_ARGTYPES = {
+    "nb_host_accel_soa": [_p] * 4 + [_i64, _d, _d, _i, _i64, _i] + [_p] * 3,
+    "nb_host_accel_aos": [_p, _p, _i64, _d, _d] + [_p] * 3,
+    "nb_host_step_soa": [_p] * 9 + [_i64, _d, _i],
+    "nb_host_step_aos": [_p] * 5 + [_i64, _d],
+    "nb_host_simulate_soa": [_p] * 7 + [_i64, _d, _d, _d, _i64],
+    "nb_dev_step": [_p, _i64, _i64, _i64, _i64, _i64, _d, _d, _d, _i, _i, _p, _i, _p, _p, _p, _p, _i64, _p],
+    "nb_dev_simulate": [_p, _p, _p, _p, _i64, _d, _d, _d, _i64, _i, _p, _i64, _p, ctypes.POINTER(_i)],
+    "nb_dev_drift": [_p, _p, _p, _i64, _d, _p],
+    "nb_dev_kick": [_p, _p, _p, _i64, _d, _p],
+    "nb_dev_energy": [_p, _p, _i64, _d, _d, _p, _p, _i64, _p],
+}
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+class NativeError(RuntimeError):
+    """A nonzero return code from libnbody_b200 (message from nb_last_error)."""
+
+    def __init__(self, func: str, code: int, message: str):
+        super().__init__(f"{func} failed with code {code}: {message}")
+        self.code = code
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: the CUDA extension has not been built "
+                "(run `python -m paper_2203_08263_b200._build`); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        for base, args in _ARGTYPES.items():
+            for sfx in ("_f32", "_f64"):
+                fn = getattr(L, base + sfx)
+                fn.argtypes = args
+                fn.restype = _i
+        L.nb_dev_workspace_bytes.argtypes = [_i, _i64]
+        L.nb_dev_workspace_bytes.restype = _i64
+        L.nb_last_error.restype = ctypes.c_char_p
+        L.nb_version.restype = ctypes.c_char_p
+        L.nb_launch_count.restype = _i64
+        _lib = L
+    return _lib
+
+
+def call(name: str, *args) -> None:
+    """Call an int-returning entry point and raise NativeError on failure."""
+    L = lib()
+    rc = getattr(L, name)(*args)
+    if rc != 0:
+        msg = L.nb_last_error()
+        raise NativeError(name, rc, msg.decode() if msg else "")
+
+
+def workspace_bytes(precision_bytes: int, n_i: int) -> int:
+    return int(lib().nb_dev_workspace_bytes(precision_bytes, n_i))
+
+
+def launch_count() -> int:
+    return int(lib().nb_launch_count())
+
+
+def version() -> str:
+    return lib().nb_version().decode()
+
+
+def declared_symbols(header: str = HEADER) -> list:
+    """Function names declared in include/nbody_b200.h."""
+    text = open(header).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(nb_[a-z0-9_]+)\s*\(", text)))

@@ -1,0 +1,434 @@
+// extern "C" boundary of libnbody_b200.so (declared in include/nbody_b200.h).
+//
+// nb_host_* mirror the reference's compiled-kernel FFI (the Cython functions of
+// /root/reference/pkg/src/nbodybench/kernels/_accel_cy.pyx) and the step loop of
+// kernels.simulate (kernels/__init__.py:230-253) on host pointers; nb_dev_* are
+// the stream-ordered device-pointer entry points the Python host code drives.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "nbody_b200.h"
+#include "nbody_kernels.h"
+
+namespace nb {
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace nb
+
+using namespace nb;
+
+namespace {
+
+thread_local std::string t_err;
+
+int fail(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  t_err = std::string(where) + ": " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e);
+  return NB_ERR_CUDA + (int)e;
+}
+#define NB_CUDA(call)                                 \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Make the device that owns `p` current for this runtime instance.  The library
+// links its own (static) CUDA runtime, whose notion of the current device need
+// not follow the host framework's (e.g. torch.cuda.set_device(local_rank)).
+cudaError_t bind_device_of(const void* p) {
+  cudaPointerAttributes attr;
+  cudaError_t e = cudaPointerGetAttributes(&attr, p);
+  if (e != cudaSuccess) return e;
+  if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged) return cudaErrorInvalidDevicePointer;
+  int cur = -1;
+  if ((e = cudaGetDevice(&cur)) != cudaSuccess) return e;
+  return cur == attr.device ? cudaSuccess : cudaSetDevice(attr.device);
+}
+
+template <typename R>
+int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
+             int64_t j_count, double g, double eps2, double dt, int mode, int exclude_self,
+             double* carry, int carry_mode, void* acc4, void* vel4, void* pos4_next,
+             void* workspace, int64_t workspace_bytes, void* stream) {
+  if (n_all < 1 || i_begin < 0 || n_i < 0 || i_begin + n_i > n_all)
+    return fail(NB_ERR_ARG, "target range [i_begin, i_begin+n_i) must lie in [0, n_all)");
+  if (j_begin < 0 || j_begin >= n_all || j_count < 0 || j_count > n_all)
+    return fail(NB_ERR_ARG, "source range must satisfy 0 <= j_begin < n_all and 0 <= j_count <= n_all");
+  if (mode < NB_MODE_ACCEL || mode > NB_STEP_FINAL_KICK)
+    return fail(NB_ERR_ARG, "mode must be NB_MODE_ACCEL or an NB_STEP_* mode");
+  if (carry_mode < 0 || carry_mode > 2) return fail(NB_ERR_ARG, "carry_mode must be 0, 1 or 2");
+  if (carry_mode != 0 && !carry) return fail(NB_ERR_ARG, "carry buffer required for carry_mode 1/2");
+  if (!(g == g) || !(eps2 >= 0.0)) return fail(NB_ERR_ARG, "g must be a number and eps2 >= 0");
+  if (n_i == 0) return NB_OK;
+  if (!pos4 || !aligned16(pos4)) return fail(NB_ERR_ARG, "pos4 must be a 16-byte aligned device pointer");
+  const bool finalize = carry_mode != 1;
+  if (finalize && (!acc4 || !aligned16(acc4))) return fail(NB_ERR_ARG, "acc4 must be a 16-byte aligned device pointer");
+  if (finalize && mode != NB_MODE_ACCEL && (!vel4 || !aligned16(vel4)))
+    return fail(NB_ERR_ARG, "vel4 required (16-byte aligned) for step modes");
+  if (finalize && (mode == NB_STEP_FIRST || mode == NB_STEP_KICK_DRIFT)) {
+    if (!pos4_next || !aligned16(pos4_next)) return fail(NB_ERR_ARG, "pos4_next required for drift modes");
+    if (pos4_next == pos4) return fail(NB_ERR_ARG, "pos4_next must not alias pos4");
+  }
+  if (cudaError_t be = bind_device_of(pos4)) return cuda_fail(be, "pos4 is not a device pointer");
+  const int64_t need = step_workspace_bytes<R>(n_i);
+  if (!workspace || workspace_bytes < need)
+    return fail(NB_ERR_WORKSPACE, "workspace smaller than nb_dev_workspace_bytes(): need " + std::to_string(need));
+
+  const StepGeometry geo = step_geometry<R>(n_i, j_count);
+  StepArgs<R> a{};
+  a.pos = static_cast<const V4<R>*>(pos4);
+  a.n_all = n_all; a.i_begin = i_begin; a.n_i = n_i; a.j_begin = j_begin; a.j_count = j_count;
+  a.eps2 = (R)eps2;
+  a.g = g;
+  a.dt = (R)dt; a.half = (R)0.5; a.f = (R)(0.5 * dt);
+  a.mode = mode; a.carry_mode = carry_mode; a.carry = carry;
+  a.acc = static_cast<V4<R>*>(acc4);
+  a.vel = static_cast<V4<R>*>(vel4);
+  a.pos_next = static_cast<V4<R>*>(pos4_next);
+  a.counters = static_cast<unsigned*>(workspace);
+  a.slots = reinterpret_cast<double*>(static_cast<char*>(workspace) + counters_bytes(geo.n_iblocks));
+  cudaError_t e = launch_step<R>(a, exclude_self != 0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "launch_step");
+  return NB_OK;
+}
+
+template <typename R>
+int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, double g, double dt,
+                 double eps2, int64_t steps, int exclude_self, void* ws, int64_t ws_bytes, void* stream,
+                 int* final_in_b) {
+  if (steps < 1) return fail(NB_ERR_ARG, "steps must be >= 1");
+  if (!(dt > 0.0)) return fail(NB_ERR_ARG, "dt must be positive");
+  void* cur = pos_a;
+  void* nxt = pos_b;
+  for (int64_t s = 0; s < steps; ++s) {
+    const int mode = s == 0 ? NB_STEP_FIRST : NB_STEP_KICK_DRIFT;
+    int rc = dev_step<R>(cur, n, 0, n, 0, n, g, eps2, dt, mode, exclude_self, nullptr, 0, acc4, vel4, nxt, ws,
+                         ws_bytes, stream);
+    if (rc) return rc;
+    void* t = cur; cur = nxt; nxt = t;
+  }
+  int rc = dev_step<R>(cur, n, 0, n, 0, n, g, eps2, dt, NB_STEP_FINAL_KICK, exclude_self, nullptr, 0, acc4,
+                       vel4, nullptr, ws, ws_bytes, stream);
+  if (rc) return rc;
+  if (final_in_b) *final_in_b = cur == pos_b ? 1 : 0;
+  return NB_OK;
+}
+
+// Whether the self pair can be included without a mask: (R)eps2 > 0 and the
+// largest self term m*eps2^-1.5 is finite with margin (else 0*inf = NaN).
+template <typename R>
+bool needs_mask(const R* m, int64_t n, double eps2) {
+  const double e = (double)(R)eps2;
+  if (!(e > 0.0)) return true;
+  double mmax = 0.0;
+  for (int64_t i = 0; i < n; ++i) mmax = m[i] > mmax ? (double)m[i] : mmax;
+  const double big = sizeof(R) == 4 ? 1e30 : 1e300;
+  const double term = mmax * (1.0 / e) / std::sqrt(e);  // FP64 evaluation of the bound
+  return !(term < big);
+}
+
+// RAII bag of device allocations for the host-pointer entry points.
+struct DevBufs {
+  void* p[12] = {};
+  int n = 0;
+  cudaError_t err = cudaSuccess;
+  void* alloc(size_t bytes) {
+    void* q = nullptr;
+    if (err == cudaSuccess) err = cudaMalloc(&q, bytes ? bytes : 16);
+    if (err == cudaSuccess) p[n++] = q;
+    return q;
+  }
+  ~DevBufs() {
+    for (int k = 0; k < n; ++k) cudaFree(p[k]);
+  }
+};
+
+template <typename R>
+int h2d(void* dst, const R* src, int64_t n) {
+  NB_CUDA(cudaMemcpy(dst, src, sizeof(R) * n, cudaMemcpyHostToDevice));
+  return NB_OK;
+}
+template <typename R>
+int d2h(R* dst, const void* src, int64_t n) {
+  NB_CUDA(cudaMemcpy(dst, src, sizeof(R) * n, cudaMemcpyDeviceToHost));
+  return NB_OK;
+}
+
+template <typename R>
+int host_accel(const R* px, const R* py, const R* pz, const R* pos_aos, const R* m, int64_t n, double g,
+               double eps2, R* ax, R* ay, R* az) {
+  if (n < 1) return fail(NB_ERR_ARG, "n must be >= 1");
+  if (!m || !ax || !ay || !az || (!pos_aos && (!px || !py || !pz))) return fail(NB_ERR_ARG, "null host pointer");
+  DevBufs B;
+  void* dm = B.alloc(sizeof(R) * n);
+  void* dpos = B.alloc(sizeof(V4<R>) * n);
+  void* dacc = B.alloc(sizeof(V4<R>) * n);
+  void* dx = B.alloc(sizeof(R) * 3 * n);
+  const int64_t wsb = step_workspace_bytes<R>(n);
+  void* ws = B.alloc(wsb);
+  if (B.err != cudaSuccess) return cuda_fail(B.err, "cudaMalloc");
+  R* d0 = static_cast<R*>(dx);
+  int rc;
+  if ((rc = h2d<R>(dm, m, n))) return rc;
+  if (pos_aos) {
+    if ((rc = h2d<R>(d0, pos_aos, 3 * n))) return rc;
+    NB_CUDA(launch_pack_aos<R>(d0, static_cast<R*>(dm), static_cast<V4<R>*>(dpos), n, 0));
+  } else {
+    if ((rc = h2d<R>(d0, px, n)) || (rc = h2d<R>(d0 + n, py, n)) || (rc = h2d<R>(d0 + 2 * n, pz, n))) return rc;
+    NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, static_cast<R*>(dm), static_cast<V4<R>*>(dpos), n, 0));
+  }
+  NB_CUDA(cudaMemset(ws, 0, wsb));
+  if ((rc = dev_step<R>(dpos, n, 0, n, 0, n, g, eps2, 0.0, NB_MODE_ACCEL, needs_mask<R>(m, n, eps2) ? 1 : 0,
+                        nullptr, 0, dacc, nullptr, nullptr, ws, wsb, nullptr)))
+    return rc;
+  NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(dacc), d0, d0 + n, d0 + 2 * n, n, 0));
+  if ((rc = d2h<R>(ax, d0, n)) || (rc = d2h<R>(ay, d0 + n, n)) || (rc = d2h<R>(az, d0 + 2 * n, n))) return rc;
+  return NB_OK;
+}
+
+template <typename R>
+int host_step(R* px, R* py, R* pz, R* vx, R* vy, R* vz, R* pos_aos, R* vel_aos, const R* ax, const R* ay,
+              const R* az, int64_t n, double dt) {
+  if (n < 1) return fail(NB_ERR_ARG, "n must be >= 1");
+  if (!ax || !ay || !az) return fail(NB_ERR_ARG, "null host pointer");
+  DevBufs B;
+  void* dpos = B.alloc(sizeof(V4<R>) * n);
+  void* dvel = B.alloc(sizeof(V4<R>) * n);
+  void* dacc = B.alloc(sizeof(V4<R>) * n);
+  void* dx = B.alloc(sizeof(R) * 3 * n);
+  if (B.err != cudaSuccess) return cuda_fail(B.err, "cudaMalloc");
+  R* d0 = static_cast<R*>(dx);
+  V4<R>* P = static_cast<V4<R>*>(dpos);
+  V4<R>* V = static_cast<V4<R>*>(dvel);
+  V4<R>* A = static_cast<V4<R>*>(dacc);
+  int rc;
+  auto up_soa = [&](const R* x, const R* y, const R* z, V4<R>* out) -> int {
+    int r;
+    if ((r = h2d<R>(d0, x, n)) || (r = h2d<R>(d0 + n, y, n)) || (r = h2d<R>(d0 + 2 * n, z, n))) return r;
+    NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, nullptr, out, n, 0));
+    return NB_OK;
+  };
+  auto down_soa = [&](const V4<R>* in, R* x, R* y, R* z) -> int {
+    NB_CUDA(launch_unpack_soa<R>(in, d0, d0 + n, d0 + 2 * n, n, 0));
+    int r;
+    if ((r = d2h<R>(x, d0, n)) || (r = d2h<R>(y, d0 + n, n)) || (r = d2h<R>(z, d0 + 2 * n, n))) return r;
+    return NB_OK;
+  };
+  auto up_aos = [&](const R* xyz, V4<R>* out) -> int {
+    int r;
+    if ((r = h2d<R>(d0, xyz, 3 * n))) return r;
+    NB_CUDA(launch_pack_aos<R>(d0, nullptr, out, n, 0));
+    return NB_OK;
+  };
+  auto down_aos = [&](const V4<R>* in, R* xyz) -> int {
+    NB_CUDA(launch_unpack_aos<R>(in, d0, n, 0));
+    return d2h<R>(xyz, d0, 3 * n);
+  };
+  if ((rc = up_soa(ax, ay, az, A))) return rc;
+  if (pos_aos) {
+    if (!vel_aos) return fail(NB_ERR_ARG, "null host pointer");
+    if ((rc = up_aos(pos_aos, P)) || (rc = up_aos(vel_aos, V))) return rc;
+  } else {
+    if (!px || !py || !pz || !vx || !vy || !vz) return fail(NB_ERR_ARG, "null host pointer");
+    if ((rc = up_soa(px, py, pz, P)) || (rc = up_soa(vx, vy, vz, V))) return rc;
+  }
+  NB_CUDA(launch_drift<R>(P, V, A, n, dt, 0));
+  if (pos_aos) {
+    if ((rc = down_aos(P, pos_aos)) || (rc = down_aos(V, vel_aos))) return rc;
+  } else {
+    if ((rc = down_soa(P, px, py, pz)) || (rc = down_soa(V, vx, vy, vz))) return rc;
+  }
+  return NB_OK;
+}
+
+template <typename R>
+int host_simulate(R* px, R* py, R* pz, R* vx, R* vy, R* vz, const R* m, int64_t n, double g, double dt,
+                  double eps2, int64_t steps) {
+  if (n < 1) return fail(NB_ERR_ARG, "n must be >= 1");
+  if (!px || !py || !pz || !vx || !vy || !vz || !m) return fail(NB_ERR_ARG, "null host pointer");
+  DevBufs B;
+  void* pa = B.alloc(sizeof(V4<R>) * n);
+  void* pb = B.alloc(sizeof(V4<R>) * n);
+  void* dv = B.alloc(sizeof(V4<R>) * n);
+  void* da = B.alloc(sizeof(V4<R>) * n);
+  void* dx = B.alloc(sizeof(R) * 4 * n);
+  const int64_t wsb = step_workspace_bytes<R>(n);
+  void* ws = B.alloc(wsb);
+  if (B.err != cudaSuccess) return cuda_fail(B.err, "cudaMalloc");
+  R* d0 = static_cast<R*>(dx);
+  int rc;
+  if ((rc = h2d<R>(d0, px, n)) || (rc = h2d<R>(d0 + n, py, n)) || (rc = h2d<R>(d0 + 2 * n, pz, n)) ||
+      (rc = h2d<R>(d0 + 3 * n, m, n)))
+    return rc;
+  NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, d0 + 3 * n, static_cast<V4<R>*>(pa), n, 0));
+  if ((rc = h2d<R>(d0, vx, n)) || (rc = h2d<R>(d0 + n, vy, n)) || (rc = h2d<R>(d0 + 2 * n, vz, n))) return rc;
+  NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, nullptr, static_cast<V4<R>*>(dv), n, 0));
+  NB_CUDA(cudaMemset(ws, 0, wsb));
+  int in_b = 0;
+  if ((rc = dev_simulate<R>(pa, pb, dv, da, n, g, dt, eps2, steps, needs_mask<R>(m, n, eps2) ? 1 : 0, ws, wsb,
+                            nullptr, &in_b)))
+    return rc;
+  NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(in_b ? pb : pa), d0, d0 + n, d0 + 2 * n, n, 0));
+  if ((rc = d2h<R>(px, d0, n)) || (rc = d2h<R>(py, d0 + n, n)) || (rc = d2h<R>(pz, d0 + 2 * n, n))) return rc;
+  NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(dv), d0, d0 + n, d0 + 2 * n, n, 0));
+  if ((rc = d2h<R>(vx, d0, n)) || (rc = d2h<R>(vy, d0 + n, n)) || (rc = d2h<R>(vz, d0 + 2 * n, n))) return rc;
+  return NB_OK;
+}
+
+template <typename R>
+int dev_drift(void* pos4, void* vel4, const void* acc4, int64_t n, double dt, void* stream) {
+  if (n < 0) return fail(NB_ERR_ARG, "n must be >= 0");
+  if (n == 0) return NB_OK;
+  if (!pos4 || !vel4 || !acc4) return fail(NB_ERR_ARG, "null device pointer");
+  if (cudaError_t be = bind_device_of(pos4)) return cuda_fail(be, "pos4 is not a device pointer");
+  NB_CUDA(launch_drift<R>(static_cast<V4<R>*>(pos4), static_cast<V4<R>*>(vel4), static_cast<const V4<R>*>(acc4), n,
+                          dt, static_cast<cudaStream_t>(stream)));
+  return NB_OK;
+}
+
+template <typename R>
+int dev_kick(void* vel4, const void* an, const void* ao, int64_t n, double factor, void* stream) {
+  if (n < 0) return fail(NB_ERR_ARG, "n must be >= 0");
+  if (n == 0) return NB_OK;
+  if (!vel4 || !an || !ao) return fail(NB_ERR_ARG, "null device pointer");
+  if (cudaError_t be = bind_device_of(vel4)) return cuda_fail(be, "vel4 is not a device pointer");
+  NB_CUDA(launch_kick<R>(static_cast<V4<R>*>(vel4), static_cast<const V4<R>*>(an), static_cast<const V4<R>*>(ao), n,
+                         factor, static_cast<cudaStream_t>(stream)));
+  return NB_OK;
+}
+
+template <typename R>
+int dev_energy(const void* pos4, const void* vel4, int64_t n, double g, double eps2, double* out6, void* ws,
+               int64_t ws_bytes, void* stream) {
+  if (n < 1) return fail(NB_ERR_ARG, "n must be >= 1");
+  if (!pos4 || !vel4 || !out6) return fail(NB_ERR_ARG, "null device pointer");
+  if (cudaError_t be = bind_device_of(pos4)) return cuda_fail(be, "pos4 is not a device pointer");
+  if (!ws || ws_bytes < 8 * n) return fail(NB_ERR_WORKSPACE, "energy needs a workspace of 8*n bytes");
+  NB_CUDA(launch_energy<R>(static_cast<const V4<R>*>(pos4), static_cast<const V4<R>*>(vel4), n, g, eps2, out6,
+                           static_cast<double*>(ws), static_cast<cudaStream_t>(stream)));
+  return NB_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int nb_host_accel_soa_f32(const float* px, const float* py, const float* pz, const float* m, int64_t n, double g,
+                          double eps2, int recip, int64_t block, int threads, float* ax, float* ay, float* az) {
+  (void)recip; (void)block; (void)threads;
+  return host_accel<float>(px, py, pz, nullptr, m, n, g, eps2, ax, ay, az);
+}
+int nb_host_accel_soa_f64(const double* px, const double* py, const double* pz, const double* m, int64_t n,
+                          double g, double eps2, int recip, int64_t block, int threads, double* ax, double* ay,
+                          double* az) {
+  (void)recip; (void)block; (void)threads;
+  return host_accel<double>(px, py, pz, nullptr, m, n, g, eps2, ax, ay, az);
+}
+int nb_host_accel_aos_f32(const float* pos, const float* m, int64_t n, double g, double eps2, float* ax, float* ay,
+                          float* az) {
+  if (!pos) return fail(NB_ERR_ARG, "null host pointer");
+  return host_accel<float>(nullptr, nullptr, nullptr, pos, m, n, g, eps2, ax, ay, az);
+}
+int nb_host_accel_aos_f64(const double* pos, const double* m, int64_t n, double g, double eps2, double* ax,
+                          double* ay, double* az) {
+  if (!pos) return fail(NB_ERR_ARG, "null host pointer");
+  return host_accel<double>(nullptr, nullptr, nullptr, pos, m, n, g, eps2, ax, ay, az);
+}
+int nb_host_step_soa_f32(float* px, float* py, float* pz, float* vx, float* vy, float* vz, const float* ax,
+                         const float* ay, const float* az, int64_t n, double dt, int threads) {
+  (void)threads;
+  return host_step<float>(px, py, pz, vx, vy, vz, nullptr, nullptr, ax, ay, az, n, dt);
+}
+int nb_host_step_soa_f64(double* px, double* py, double* pz, double* vx, double* vy, double* vz, const double* ax,
+                         const double* ay, const double* az, int64_t n, double dt, int threads) {
+  (void)threads;
+  return host_step<double>(px, py, pz, vx, vy, vz, nullptr, nullptr, ax, ay, az, n, dt);
+}
+int nb_host_step_aos_f32(float* pos, float* vel, const float* ax, const float* ay, const float* az, int64_t n,
+                         double dt) {
+  if (!pos) return fail(NB_ERR_ARG, "null host pointer");
+  return host_step<float>(nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, pos, vel, ax, ay, az, n, dt);
+}
+int nb_host_step_aos_f64(double* pos, double* vel, const double* ax, const double* ay, const double* az, int64_t n,
+                         double dt) {
+  if (!pos) return fail(NB_ERR_ARG, "null host pointer");
+  return host_step<double>(nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, pos, vel, ax, ay, az, n, dt);
+}
+int nb_host_simulate_soa_f32(float* px, float* py, float* pz, float* vx, float* vy, float* vz, const float* m,
+                             int64_t n, double g, double dt, double eps2, int64_t steps) {
+  return host_simulate<float>(px, py, pz, vx, vy, vz, m, n, g, dt, eps2, steps);
+}
+int nb_host_simulate_soa_f64(double* px, double* py, double* pz, double* vx, double* vy, double* vz,
+                             const double* m, int64_t n, double g, double dt, double eps2, int64_t steps) {
+  return host_simulate<double>(px, py, pz, vx, vy, vz, m, n, g, dt, eps2, steps);
+}
+
+int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i) {
+  if (n_i < 1) n_i = 1;
+  if (precision_bytes == 4) return step_workspace_bytes<float>(n_i);
+  if (precision_bytes == 8) return step_workspace_bytes<double>(n_i);
+  fail(NB_ERR_ARG, "precision_bytes must be 4 or 8");
+  return -1;
+}
+
+int nb_dev_step_f32(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin, int64_t j_count,
+                    double g, double eps2, double dt, int mode, int exclude_self, double* carry, int carry_mode,
+                    void* acc4, void* vel4, void* pos4_next, void* workspace, int64_t workspace_bytes,
+                    void* stream) {
+  return dev_step<float>(pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, exclude_self, carry,
+                         carry_mode, acc4, vel4, pos4_next, workspace, workspace_bytes, stream);
+}
+int nb_dev_step_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin, int64_t j_count,
+                    double g, double eps2, double dt, int mode, int exclude_self, double* carry, int carry_mode,
+                    void* acc4, void* vel4, void* pos4_next, void* workspace, int64_t workspace_bytes,
+                    void* stream) {
+  return dev_step<double>(pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, exclude_self, carry,
+                          carry_mode, acc4, vel4, pos4_next, workspace, workspace_bytes, stream);
+}
+int nb_dev_simulate_f32(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n, double g, double dt,
+                        double eps2, int64_t steps, int exclude_self, void* workspace, int64_t workspace_bytes,
+                        void* stream, int* final_in_b) {
+  return dev_simulate<float>(pos4_a, pos4_b, vel4, acc4, n, g, dt, eps2, steps, exclude_self, workspace,
+                             workspace_bytes, stream, final_in_b);
+}
+int nb_dev_simulate_f64(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n, double g, double dt,
+                        double eps2, int64_t steps, int exclude_self, void* workspace, int64_t workspace_bytes,
+                        void* stream, int* final_in_b) {
+  return dev_simulate<double>(pos4_a, pos4_b, vel4, acc4, n, g, dt, eps2, steps, exclude_self, workspace,
+                              workspace_bytes, stream, final_in_b);
+}
+int nb_dev_drift_f32(void* pos4, void* vel4, const void* acc4, int64_t n, double dt, void* stream) {
+  return dev_drift<float>(pos4, vel4, acc4, n, dt, stream);
+}
+int nb_dev_drift_f64(void* pos4, void* vel4, const void* acc4, int64_t n, double dt, void* stream) {
+  return dev_drift<double>(pos4, vel4, acc4, n, dt, stream);
+}
+int nb_dev_kick_f32(void* vel4, const void* an, const void* ao, int64_t n, double factor, void* stream) {
+  return dev_kick<float>(vel4, an, ao, n, factor, stream);
+}
+int nb_dev_kick_f64(void* vel4, const void* an, const void* ao, int64_t n, double factor, void* stream) {
+  return dev_kick<double>(vel4, an, ao, n, factor, stream);
+}
+int nb_dev_energy_f32(const void* pos4, const void* vel4, int64_t n, double g, double eps2, double* out6, void* ws,
+                      int64_t ws_bytes, void* stream) {
+  return dev_energy<float>(pos4, vel4, n, g, eps2, out6, ws, ws_bytes, stream);
+}
+int nb_dev_energy_f64(const void* pos4, const void* vel4, int64_t n, double g, double eps2, double* out6, void* ws,
+                      int64_t ws_bytes, void* stream) {
+  return dev_energy<double>(pos4, vel4, n, g, eps2, out6, ws, ws_bytes, stream);
+}
+
+const char* nb_last_error(void) { return t_err.c_str(); }
+const char* nb_version(void) { return "nbody_b200 0.1.0 (sm_100a)"; }
+int64_t nb_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// Internal interface between the C ABI (nbody_capi.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nbody_common.cuh"
+
+namespace nb {
+
+enum : int {
+  NB_STEP_MODE_ACCEL = 0,
+  NB_STEP_MODE_FIRST = 1,
+  NB_STEP_MODE_KICK_DRIFT = 2,
+  NB_STEP_MODE_FINAL = 3,
+};
+
+template <typename R>
+struct StepArgs {
+  const V4<R>* pos;  // n_all packed (x,y,z,m): read-only during the launch
+  int64_t n_all, i_begin, n_i, j_begin, j_count;
+  R eps2;            // (R)eps2  (_accel_cy.pyx:119)
+  double g;          // applied to the FP64 sum, then rounded to R
+  R dt, half, f;     // (R)dt, (R)0.5, (R)(0.5*dt)  (_accel_cy.pyx:211-212; __init__.py:223)
+  int mode, carry_mode;
+  double* carry;     // 3*n_i FP64 partial sums (SoA), carry_mode 1/2
+  V4<R>* acc;        // n_i: a_prev in, a out
+  V4<R>* vel;        // n_i
+  V4<R>* pos_next;   // n_all: rows of this shard written by drift modes
+  double* slots;     // stream-K partial slots (workspace)
+  unsigned* counters;  // per i-block arrival counters (workspace, zero between launches)
+  int64_t units, n_tiles, n_iblocks;
+  int64_t grid;
+};
+
+struct StepGeometry {
+  int threads, i_block, tile;
+  int64_t n_iblocks, n_tiles, units;
+};
+
+template <typename R> StepGeometry step_geometry(int64_t n_i, int64_t j_count);
+template <typename R> cudaError_t launch_step(StepArgs<R> a, bool mask_self, cudaStream_t s);
+template <typename R> int64_t step_workspace_bytes(int64_t n_i);
+// Byte offset of the slot area inside the workspace (counters come first).
+inline int64_t counters_bytes(int64_t n_iblocks) { return ((n_iblocks * 4 + 255) / 256) * 256; }
+
+// Stand-alone O(N) kernels (nbody_update.cu).
+template <typename R> cudaError_t launch_drift(V4<R>* pos, V4<R>* vel, const V4<R>* acc, int64_t n, double dt, cudaStream_t s);
+template <typename R> cudaError_t launch_kick(V4<R>* vel, const V4<R>* an, const V4<R>* ao, int64_t n, double factor, cudaStream_t s);
+template <typename R> cudaError_t launch_pack_soa(const R* x, const R* y, const R* z, const R* w, V4<R>* out, int64_t n, cudaStream_t s);
+template <typename R> cudaError_t launch_unpack_soa(const V4<R>* in, R* x, R* y, R* z, int64_t n, cudaStream_t s);
+template <typename R> cudaError_t launch_pack_aos(const R* xyz, const R* w, V4<R>* out, int64_t n, cudaStream_t s);
+template <typename R> cudaError_t launch_unpack_aos(const V4<R>* in, R* xyz, int64_t n, cudaStream_t s);
+template <typename R> cudaError_t launch_energy(const V4<R>* pos, const V4<R>* vel, int64_t n, double g, double eps2,
+                                                double* out6, double* phi, cudaStream_t s);
+
+}  // namespace nb

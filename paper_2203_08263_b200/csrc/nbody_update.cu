@@ -1,0 +1,201 @@
+// O(N) kernels around the force pass: the stand-alone kick-drift and kick
+// updates, SoA/AoS <-> packed conversion at the boundary, and the FP64 energy
+// diagnostics.  All are HBM-bound and negligible next to the O(N^2) pass.
+#include "nbody_common.cuh"
+#include "nbody_kernels.h"
+
+namespace nb {
+
+static inline int blocks_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  return (int)(b < 1 ? 1 : (b > (1 << 30) ? (1 << 30) : b));
+}
+
+// step_soa (_accel_cy.pyx:205-237): dv = a*dt; p += (v + half*dv)*dt; v += dv,
+// every operation individually rounded (no contraction), dt and half in R.
+template <typename R>
+__global__ void drift_kernel(V4<R>* pos, V4<R>* vel, const V4<R>* acc, int64_t n, R dt) {
+  const R half = R(0.5);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    V4<R> p = pos[i], v = vel[i];
+    const V4<R> a = acc[i];
+    const R dvx = mul_rn(a.x, dt), dvy = mul_rn(a.y, dt), dvz = mul_rn(a.z, dt);
+    p.x = add_rn(p.x, mul_rn(add_rn(v.x, mul_rn(half, dvx)), dt));
+    p.y = add_rn(p.y, mul_rn(add_rn(v.y, mul_rn(half, dvy)), dt));
+    p.z = add_rn(p.z, mul_rn(add_rn(v.z, mul_rn(half, dvz)), dt));
+    v.x = add_rn(v.x, dvx);
+    v.y = add_rn(v.y, dvy);
+    v.z = add_rn(v.z, dvz);
+    st4(pos + i, p);
+    st4(vel + i, v);
+  }
+}
+
+// _kick (kernels/__init__.py:220-227): v += (new - old) * f, f = R(factor).
+template <typename R>
+__global__ void kick_kernel(V4<R>* vel, const V4<R>* an, const V4<R>* ao, int64_t n, R f) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    V4<R> v = vel[i];
+    const V4<R> a1 = an[i], a0 = ao[i];
+    v.x = add_rn(v.x, mul_rn(sub_rn(a1.x, a0.x), f));
+    v.y = add_rn(v.y, mul_rn(sub_rn(a1.y, a0.y), f));
+    v.z = add_rn(v.z, mul_rn(sub_rn(a1.z, a0.z), f));
+    st4(vel + i, v);
+  }
+}
+
+template <typename R>
+__global__ void pack_soa_kernel(const R* x, const R* y, const R* z, const R* w, V4<R>* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    V4<R> v;
+    v.x = x[i]; v.y = y[i]; v.z = z[i]; v.w = w ? w[i] : R(0);
+    st4(out + i, v);
+  }
+}
+
+template <typename R>
+__global__ void unpack_soa_kernel(const V4<R>* in, R* x, R* y, R* z, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const V4<R> v = in[i];
+    x[i] = v.x; y[i] = v.y; z[i] = v.z;
+  }
+}
+
+template <typename R>
+__global__ void pack_aos_kernel(const R* xyz, const R* w, V4<R>* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    V4<R> v;
+    v.x = xyz[3 * i]; v.y = xyz[3 * i + 1]; v.z = xyz[3 * i + 2]; v.w = w ? w[i] : R(0);
+    st4(out + i, v);
+  }
+}
+
+template <typename R>
+__global__ void unpack_aos_kernel(const V4<R>* in, R* xyz, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const V4<R> v = in[i];
+    xyz[3 * i] = v.x; xyz[3 * i + 1] = v.y; xyz[3 * i + 2] = v.z;
+  }
+}
+
+// Potential per body, phi_i = sum_{j != i} m_j / sqrt(|p_j - p_i|^2 + eps2), FP64.
+template <typename R>
+__global__ void __launch_bounds__(256) potential_kernel(const V4<R>* pos, int64_t n, double eps2, double* phi) {
+  __shared__ double4 tile[256];
+  const int64_t i = blockIdx.x * 256LL + threadIdx.x;
+  const V4<R> pi = pos[i < n ? i : n - 1];
+  const double xi = pi.x, yi = pi.y, zi = pi.z;
+  double s = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += 256) {
+    const int64_t j = j0 + threadIdx.x;
+    if (j < n) {
+      const V4<R> pj = pos[j];
+      tile[threadIdx.x] = make_double4(pj.x, pj.y, pj.z, pj.w);
+    }
+    __syncthreads();
+    const int cnt = (int)(n - j0 < 256 ? n - j0 : 256);
+    for (int jj = 0; jj < cnt; ++jj) {
+      const double4 q = tile[jj];
+      const double dx = q.x - xi, dy = q.y - yi, dz = q.z - zi;
+      const double t = q.w * rsqrt(dx * dx + dy * dy + dz * dz + eps2);
+      s += (j0 + jj == i) ? 0.0 : t;
+    }
+    __syncthreads();
+  }
+  if (i < n) phi[i] = s;
+}
+
+// Fixed-order block reduction: out6 = (KE, PE, Px, Py, Pz, KE+PE).
+template <typename R>
+__global__ void __launch_bounds__(1024) energy_reduce_kernel(const V4<R>* pos, const V4<R>* vel, const double* phi,
+                                                             int64_t n, double g, double* out6) {
+  __shared__ double red[5][1024];
+  double ke = 0, pe = 0, px = 0, py = 0, pz = 0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) {
+    const double m = pos[i].w;
+    const V4<R> v = vel[i];
+    const double vx = v.x, vy = v.y, vz = v.z;
+    ke += 0.5 * m * (vx * vx + vy * vy + vz * vz);
+    pe += m * phi[i];
+    px += m * vx; py += m * vy; pz += m * vz;
+  }
+  red[0][threadIdx.x] = ke; red[1][threadIdx.x] = pe;
+  red[2][threadIdx.x] = px; red[3][threadIdx.x] = py; red[4][threadIdx.x] = pz;
+  __syncthreads();
+  for (int s = 512; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int k = 0; k < 5; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double KE = red[0][0], PE = -0.5 * g * red[1][0];
+    out6[0] = KE; out6[1] = PE; out6[2] = red[2][0]; out6[3] = red[3][0]; out6[4] = red[4][0];
+    out6[5] = KE + PE;
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+template <typename R>
+cudaError_t launch_drift(V4<R>* pos, V4<R>* vel, const V4<R>* acc, int64_t n, double dt, cudaStream_t s) {
+  drift_kernel<R><<<blocks_for(n, 256), 256, 0, s>>>(pos, vel, acc, n, (R)dt);
+  count_launch();
+  return cudaGetLastError();
+}
+template <typename R>
+cudaError_t launch_kick(V4<R>* vel, const V4<R>* an, const V4<R>* ao, int64_t n, double factor, cudaStream_t s) {
+  kick_kernel<R><<<blocks_for(n, 256), 256, 0, s>>>(vel, an, ao, n, (R)factor);
+  count_launch();
+  return cudaGetLastError();
+}
+template <typename R>
+cudaError_t launch_pack_soa(const R* x, const R* y, const R* z, const R* w, V4<R>* out, int64_t n, cudaStream_t s) {
+  pack_soa_kernel<R><<<blocks_for(n, 256), 256, 0, s>>>(x, y, z, w, out, n);
+  count_launch();
+  return cudaGetLastError();
+}
+template <typename R>
+cudaError_t launch_unpack_soa(const V4<R>* in, R* x, R* y, R* z, int64_t n, cudaStream_t s) {
+  unpack_soa_kernel<R><<<blocks_for(n, 256), 256, 0, s>>>(in, x, y, z, n);
+  count_launch();
+  return cudaGetLastError();
+}
+template <typename R>
+cudaError_t launch_pack_aos(const R* xyz, const R* w, V4<R>* out, int64_t n, cudaStream_t s) {
+  pack_aos_kernel<R><<<blocks_for(n, 256), 256, 0, s>>>(xyz, w, out, n);
+  count_launch();
+  return cudaGetLastError();
+}
+template <typename R>
+cudaError_t launch_unpack_aos(const V4<R>* in, R* xyz, int64_t n, cudaStream_t s) {
+  unpack_aos_kernel<R><<<blocks_for(n, 256), 256, 0, s>>>(in, xyz, n);
+  count_launch();
+  return cudaGetLastError();
+}
+template <typename R>
+cudaError_t launch_energy(const V4<R>* pos, const V4<R>* vel, int64_t n, double g, double eps2, double* out6,
+                          double* phi, cudaStream_t s) {
+  potential_kernel<R><<<blocks_for(n, 256), 256, 0, s>>>(pos, n, eps2, phi);
+  energy_reduce_kernel<R><<<1, 1024, 0, s>>>(pos, vel, phi, n, g, out6);
+  count_launch(2);
+  return cudaGetLastError();
+}
+
+#define NB_INST(R)                                                                                  \
+  template cudaError_t launch_drift<R>(V4<R>*, V4<R>*, const V4<R>*, int64_t, double, cudaStream_t); \
+  template cudaError_t launch_kick<R>(V4<R>*, const V4<R>*, const V4<R>*, int64_t, double, cudaStream_t); \
+  template cudaError_t launch_pack_soa<R>(const R*, const R*, const R*, const R*, V4<R>*, int64_t, cudaStream_t); \
+  template cudaError_t launch_unpack_soa<R>(const V4<R>*, R*, R*, R*, int64_t, cudaStream_t);       \
+  template cudaError_t launch_pack_aos<R>(const R*, const R*, V4<R>*, int64_t, cudaStream_t);       \
+  template cudaError_t launch_unpack_aos<R>(const V4<R>*, R*, int64_t, cudaStream_t);               \
+  template cudaError_t launch_energy<R>(const V4<R>*, const V4<R>*, int64_t, double, double, double*, double*, cudaStream_t);
+NB_INST(float)
+NB_INST(double)
+#undef NB_INST
+
+}  // namespace nb

@@ -1,0 +1,162 @@
+"""Device-resident state and the GPU driver for one device.
+
+PyTorch is used only for what it is good at here: device allocation, pinned
+host staging and the CUDA stream handle.  All arithmetic runs in the sm_100a
+kernels behind libnbody_b200.so (``_native``).
+
+HBM layout (one GPU, or one i-shard of a multi-GPU run):
+
+* ``pos_a``, ``pos_b`` -- (N, 4) packed (x, y, z, m), ping-ponged between steps
+  (the force pass reads all N while the fused epilogue writes the next
+  positions of its own rows, so the two must not alias);
+* ``vel``, ``acc`` -- (n_i, 4) for the target rows only; ``acc`` holds the
+  previous step's accelerations for the trapezoidal kick;
+* ``carry`` -- (3, n_i) FP64 partial sums for a split source range;
+* ``ws`` -- the stream-K workspace (arrival counters + FP64 partial slots),
+  zero-filled once and left zeroed by every launch.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _native
+from ._native import NB_MODE_ACCEL, NB_STEP_FINAL_KICK, NB_STEP_FIRST, NB_STEP_KICK_DRIFT
+
+__all__ = ["DeviceState", "needs_self_mask", "pack_bodies", "TORCH_DTYPE"]
+
+TORCH_DTYPE = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
+
+
+def needs_self_mask(masses: np.ndarray, eps2: float, dtype) -> bool:
+    """True when the self pair must be excluded explicitly: (real)eps2 == 0
+    (0*inf at j == i, the case pinned by pkg/tests/test_kernels.py:51-55), or a
+    self term m*eps2^-1.5 that would overflow the system precision."""
+    dtype = np.dtype(dtype)
+    e = float(dtype.type(eps2))
+    if not e > 0.0:
+        return True
+    big = 1e30 if dtype == np.float32 else 1e300
+    mmax = float(np.max(masses)) if masses.size else 0.0
+    return not (mmax * (1.0 / e) / np.sqrt(e) < big)
+
+
+def pack_bodies(pos: np.ndarray, w: Optional[np.ndarray], dtype, pin: bool) -> torch.Tensor:
+    """(N,3) coordinates (+ optional 4th column) -> (N,4) host tensor, pinned if asked."""
+    n = pos.shape[0]
+    t = torch.empty((n, 4), dtype=TORCH_DTYPE[np.dtype(dtype)], pin_memory=pin)
+    a = t.numpy()
+    a[:, :3] = pos
+    a[:, 3] = 0 if w is None else w
+    return t
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class DeviceState:
+    """Packed device buffers for the target rows [i_begin, i_begin+n_i) of an
+    N-body system (all N positions are resident: every target needs every source)."""
+
+    def __init__(self, positions: np.ndarray, velocities: np.ndarray, masses: np.ndarray, dtype,
+                 device: Optional[torch.device] = None, i_begin: int = 0, n_i: Optional[int] = None,
+                 eps2_hint: Optional[float] = None):
+        self.dtype = np.dtype(dtype)
+        if self.dtype not in TORCH_DTYPE:
+            raise ValueError(f"unsupported precision {self.dtype}")
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise RuntimeError("DeviceState needs a CUDA device; there is no CPU fallback")
+        self.n = int(positions.shape[0])
+        self.i_begin = int(i_begin)
+        self.n_i = self.n - self.i_begin if n_i is None else int(n_i)
+        self.sfx = "_f32" if self.dtype == np.float32 else "_f64"
+        self.pbytes = self.dtype.itemsize
+        self.masses = np.ascontiguousarray(masses, dtype=self.dtype)
+        tdt = TORCH_DTYPE[self.dtype]
+        host_pos = pack_bodies(np.asarray(positions, self.dtype), self.masses, self.dtype, pin=True)
+        host_vel = pack_bodies(np.asarray(velocities, self.dtype)[self.i_begin:self.i_begin + self.n_i],
+                               None, self.dtype, pin=True)
+        self.pos_a = host_pos.to(self.device, non_blocking=True)
+        self.pos_b = torch.empty_like(self.pos_a)
+        self.vel = host_vel.to(self.device, non_blocking=True)
+        self.acc = torch.zeros((max(self.n_i, 1), 4), dtype=tdt, device=self.device)
+        self.carry = torch.zeros((3, max(self.n_i, 1)), dtype=torch.float64, device=self.device)
+        self.ws_bytes = _native.workspace_bytes(self.pbytes, max(self.n_i, 1))
+        self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.cur_is_a = True
+        self._host_keepalive = (host_pos, host_vel)
+
+    # -------------------------------------------------------------- buffers
+    @property
+    def pos_cur(self) -> torch.Tensor:
+        return self.pos_a if self.cur_is_a else self.pos_b
+
+    @property
+    def pos_next(self) -> torch.Tensor:
+        return self.pos_b if self.cur_is_a else self.pos_a
+
+    def swap(self) -> None:
+        self.cur_is_a = not self.cur_is_a
+
+    def stream_ptr(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    # -------------------------------------------------------------- kernels
+    def step(self, g: float, eps2: float, dt: float, mode: int, exclude_self: bool,
+             j_begin: Optional[int] = None, j_count: Optional[int] = None, carry_mode: int = 0,
+             acc_out: Optional[torch.Tensor] = None) -> None:
+        """One fused force(+update) launch on the current positions (nb_dev_step)."""
+        j_begin = self.i_begin if j_begin is None else j_begin
+        j_count = self.n if j_count is None else j_count
+        acc = self.acc if acc_out is None else acc_out
+        drift = mode in (NB_STEP_FIRST, NB_STEP_KICK_DRIFT)
+        _native.call("nb_dev_step" + self.sfx, self.pos_cur.data_ptr(), self.n, self.i_begin, self.n_i,
+                     j_begin % self.n, j_count, g, eps2, dt, mode, int(exclude_self),
+                     self.carry.data_ptr() if carry_mode else None, carry_mode, acc.data_ptr(),
+                     self.vel.data_ptr() if mode != NB_MODE_ACCEL else None,
+                     self.pos_next.data_ptr() if drift else None,
+                     self.ws.data_ptr(), self.ws_bytes, self.stream_ptr())
+
+    def simulate(self, g: float, dt: float, eps2: float, steps: int, exclude_self: bool) -> None:
+        """Whole single-device velocity-Verlet run (nb_dev_simulate): steps+1 launches."""
+        if self.i_begin != 0 or self.n_i != self.n:
+            raise ValueError("DeviceState.simulate runs an unsharded system; use sharded.simulate")
+        final_in_b = ctypes.c_int(0)
+        _native.call("nb_dev_simulate" + self.sfx, self.pos_cur.data_ptr(), self.pos_next.data_ptr(),
+                     self.vel.data_ptr(), self.acc.data_ptr(), self.n, g, dt, eps2, steps,
+                     int(exclude_self), self.ws.data_ptr(), self.ws_bytes, self.stream_ptr(),
+                     ctypes.byref(final_in_b))
+        if steps % 2 == 1:
+            self.swap()
+
+    def accelerations(self, g: float, eps2: float, exclude_self: bool) -> torch.Tensor:
+        """(n_i, 4) device accelerations of the current positions (mode ACCEL)."""
+        out = torch.empty((max(self.n_i, 1), 4), dtype=self.acc.dtype, device=self.device)
+        self.step(g, eps2, 0.0, NB_MODE_ACCEL, exclude_self, j_begin=0, j_count=self.n, acc_out=out)
+        return out[: self.n_i]
+
+    def energy(self, g: float, eps2: float) -> Tuple[float, float, Tuple[float, float, float]]:
+        """(kinetic, potential, momentum) in FP64 (unsharded state only)."""
+        if self.n_i != self.n:
+            raise ValueError("energy diagnostics need the whole system on one device")
+        out = torch.zeros(6, dtype=torch.float64, device=self.device)
+        ws = torch.empty(8 * self.n, dtype=torch.uint8, device=self.device)
+        _native.call("nb_dev_energy" + self.sfx, self.pos_cur.data_ptr(), self.vel.data_ptr(), self.n,
+                     g, eps2, out.data_ptr(), ws.data_ptr(), ws.numel(), self.stream_ptr())
+        v = out.cpu().numpy()
+        return float(v[0]), float(v[1]), (float(v[2]), float(v[3]), float(v[4]))
+
+    # -------------------------------------------------------------- host views
+    def positions_host(self) -> np.ndarray:
+        return self.pos_cur[:, :3].cpu().numpy()
+
+    def velocities_host(self) -> np.ndarray:
+        return self.vel[: self.n_i, :3].cpu().numpy()

@@ -1,0 +1,121 @@
+"""i-body sharding across GPUs: one process per GPU, NCCL all-gather of positions.
+
+The reference parallelises only over target bodies i (OpenMP static schedule,
+/root/reference/pkg/src/nbodybench/kernels/_accel_cy.pyx:132-136), each worker
+writing its own slice.  Across GPUs the same axis shards: rank r
+owns the contiguous rows [r*N/P, (r+1)*N/P), keeps all N positions resident,
+and after every drift the ranks exchange their new position rows with one
+in-place all-gather (the only data-path collective; masses ride in .w).
+
+Overlap: the force pass of step k+1 first sums over the rank's OWN rows as
+sources (already valid locally) into an FP64 carry, while the all-gather of
+step k's positions is in flight on NCCL's stream; the compute stream then waits
+for the gather and sums the remaining N - N/P sources (one circular range
+starting after the local slice) before the fused update.
+
+The driver is written against a small state interface (``DeviceState``) and an
+``allgather(full, local)`` callable, so its host logic is exercised on CPU with
+gloo and an oracle-backed state in tests/test_sharded_cpu.py.
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Optional, Tuple
+
+import numpy as np
+
+from ._native import NB_STEP_FINAL_KICK, NB_STEP_FIRST, NB_STEP_KICK_DRIFT
+
+__all__ = ["shard_range", "padded_count", "run_sharded", "simulate_sharded"]
+
+
+def padded_count(n: int, world: int) -> int:
+    """Bodies after padding N up to a multiple of the world size (equal shards
+    are what an in-place all-gather needs)."""
+    return ((n + world - 1) // world) * world
+
+
+def shard_range(n_padded: int, rank: int, world: int) -> Tuple[int, int]:
+    per = n_padded // world
+    return rank * per, per
+
+
+def pad_system(pos: np.ndarray, vel: np.ndarray, m: np.ndarray, world: int):
+    """Pad to equal shards with massless bodies far from everything: they add
+    exactly 0 to every real body (w = 0 * r^3 with finite r) and their own rows
+    are discarded."""
+    n = pos.shape[0]
+    npad = padded_count(n, world)
+    if npad == n:
+        return pos, vel, m
+    extra = npad - n
+    far = np.float64(1e18) if pos.dtype == np.float64 else np.float32(1e17)
+    pad_pos = np.full((extra, 3), far, dtype=pos.dtype) * (1 + np.arange(extra, dtype=pos.dtype))[:, None]
+    return (np.concatenate([pos, pad_pos]), np.concatenate([vel, np.zeros((extra, 3), vel.dtype)]),
+            np.concatenate([m, np.zeros(extra, m.dtype)]))
+
+
+def run_sharded(state, g: float, dt: float, eps2: float, steps: int, exclude_self: bool,
+                allgather: Callable, world: int) -> None:
+    """Velocity-Verlet loop of kernels.simulate (kernels/__init__.py:240-252) on
+    one shard.  ``state`` holds all positions and this rank's rows; ``allgather``
+    starts an in-place gather of ``pos[i0:i0+ni]`` into ``pos`` on every rank and
+    returns an object with ``wait()``."""
+    n, i0, ni = state.n, state.i_begin, state.n_i
+    if world == 1:
+        for s in range(steps):
+            state.step(g, eps2, dt, NB_STEP_FIRST if s == 0 else NB_STEP_KICK_DRIFT, exclude_self)
+            state.swap()
+        state.step(g, eps2, dt, NB_STEP_FINAL_KICK, exclude_self)
+        return
+    pending = None
+    for s in range(steps + 1):
+        mode = NB_STEP_FIRST if s == 0 else (NB_STEP_KICK_DRIFT if s < steps else NB_STEP_FINAL_KICK)
+        # local sources first: rows [i0, i0+ni) of the current positions are ours
+        state.step(g, eps2, dt, mode, exclude_self, j_begin=i0, j_count=ni, carry_mode=1)
+        if pending is not None:
+            pending.wait()
+        # then every other source, as one circular range after the local slice
+        state.step(g, eps2, dt, mode, exclude_self, j_begin=(i0 + ni) % n, j_count=n - ni, carry_mode=2)
+        if mode != NB_STEP_FINAL_KICK:
+            state.swap()
+            pending = allgather(state.pos_cur, state.pos_cur[i0:i0 + ni])
+    if pending is not None:
+        pending.wait()
+
+
+def _torch_allgather(group):
+    import torch.distributed as dist
+
+    def gather(full, local):
+        return dist.all_gather_into_tensor(full, local, group=group, async_op=True)
+    return gather
+
+
+def simulate_sharded(positions: np.ndarray, velocities: np.ndarray, masses: np.ndarray, dtype,
+                     g: float, dt: float, eps2: float, steps: int, group=None,
+                     exclude_self: Optional[bool] = None) -> Tuple[np.ndarray, np.ndarray]:
+    """Multi-GPU simulate: every rank passes the full initial state and gets the
+    full final (positions, velocities) back.  Uses the default process group
+    (NCCL, one process per GPU) unless ``group`` is given."""
+    import torch
+    import torch.distributed as dist
+
+    from .device import DeviceState, needs_self_mask
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n = positions.shape[0]
+    dtype = np.dtype(dtype)
+    pos, vel, m = pad_system(np.asarray(positions, dtype), np.asarray(velocities, dtype),
+                             np.asarray(masses, dtype), world)
+    npad = pos.shape[0]
+    i0, ni = shard_range(npad, rank, world)
+    if exclude_self is None:
+        exclude_self = needs_self_mask(m[:n], eps2, dtype)
+    state = DeviceState(pos, vel, m, dtype, i_begin=i0, n_i=ni)
+    run_sharded(state, g, dt, eps2, steps, exclude_self, _torch_allgather(group), world)
+    vel_full = torch.empty((npad, 4), dtype=state.vel.dtype, device=state.device)
+    dist.all_gather_into_tensor(vel_full, state.vel[:ni].contiguous(), group=group)
+    out_pos = state.pos_cur[:n, :3].cpu().numpy()
+    out_vel = vel_full[:n, :3].cpu().numpy()
+    return out_pos, out_vel

@@ -1,0 +1,445 @@
+"""GPU parity tests: the sm_100a path (through the package API and the C ABI)
+against the CPU oracle and the reference's golden values.  Run on a B200:
+``python -m pytest tests -m gpu``.
+
+Tolerances (BASELINE.json north_star):
+  * per-step accelerations, the `_accel_dev` metric of validation.py:212-225:
+    <= 1e-5 (FP32) / <= 1e-12 (FP64) against an FP64-or-better oracle on the
+    same rounded inputs;
+  * trajectories, the `_position_dev` metric of validation.py:204-209: FP64
+    <= 1e-12; FP32 <= 10x the reference's own FP32-vs-FP64 deviation;
+  * the update arithmetic is bit-exact (same rounding sequence as step_soa/_kick).
+"""
+import numpy as np
+import pytest
+
+import paper_2203_08263_b200 as nb
+from paper_2203_08263_b200 import _native
+from paper_2203_08263_b200.core import uniform_cube
+
+pytestmark = pytest.mark.gpu
+
+F64_ACC_TOL = 1e-12
+F32_ACC_TOL = 1e-5
+F64_POS_TOL = 1e-12
+
+EPS0 = nb.SimParams(1.0, 0.1, 0.0, 1)
+
+
+def accel_of(sys_, params, variant=None):
+    out = nb.AccelerationBuffer.allocate(sys_.count, sys_.precision)
+    nb.compute_accelerations(sys_, params, variant, out)
+    return out
+
+
+def as_mat(buf):
+    return np.stack([buf.x, buf.y, buf.z], axis=1)
+
+
+def two_body(precision=nb.Precision.DOUBLE, layout=nb.Layout.SOA):
+    return nb.system_from_arrays([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0]], np.zeros((2, 3)), [1.0, 1.0],
+                                 layout=layout, precision=precision)
+
+
+def cube(n, seed, prec):
+    return uniform_cube(n, seed, nb.Precision(prec))
+
+
+# --------------------------------------------------------------------------- known answers
+# pkg/tests/test_kernels.py:22-55 restated for the GPU.
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("eps2", [0.0, 1e-3])
+def test_single_body_zero_acceleration(prec, eps2):
+    s = nb.system_from_arrays([[0.3, 0.4, 0.5]], np.zeros((1, 3)), [2.5], precision=prec)
+    a = accel_of(s, nb.SimParams(1.0, 0.1, eps2, 1))
+    assert a.x[0] == 0.0 and a.y[0] == 0.0 and a.z[0] == 0.0
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_two_body_unit_case(prec):
+    a = accel_of(two_body(nb.Precision(prec)), EPS0)
+    tol = 2.3e-16 if prec == "double" else 1.2e-7
+    np.testing.assert_allclose([a.x[0], a.x[1]], [1.0, -1.0], rtol=tol, atol=0)
+    assert np.all(a.y == 0.0) and np.all(a.z == 0.0)
+
+
+def test_unit_square_corner():
+    s = nb.system_from_arrays([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0], [1.0, 1.0, 0.0]],
+                              np.zeros((4, 3)), np.ones(4))
+    a = accel_of(s, EPS0)
+    expect = 1.0 + 2.0 ** -1.5
+    np.testing.assert_allclose(a.x[0], expect, rtol=1e-15)
+    np.testing.assert_allclose(a.y[0], expect, rtol=1e-15)
+    assert a.z[0] == 0.0
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_coincident_bodies_without_softening_are_non_finite(prec):
+    s = nb.system_from_arrays([[0.5, 0.5, 0.5], [0.5, 0.5, 0.5]], np.zeros((2, 3)), [1.0, 1.0],
+                              precision=prec)
+    a = accel_of(s, EPS0)
+    assert not np.all(np.isfinite(a.x))
+
+
+def test_buffer_checks_match_reference():
+    s = two_body()
+    with pytest.raises(ValueError):
+        nb.compute_accelerations(s, EPS0, nb.reference_variant(), nb.AccelerationBuffer.allocate(3, "double"))
+    with pytest.raises(ValueError):
+        nb.compute_accelerations(s, EPS0, nb.reference_variant(), nb.AccelerationBuffer.allocate(2, "single"))
+
+
+# --------------------------------------------------------------------------- golden cases
+
+def test_golden_case_accelerations(golden_cases, golden_arrays):
+    worst = {}
+    for c in golden_cases:
+        s = cube(c["n"], c["seed"], c["precision"])
+        a = as_mat(accel_of(s, nb.SimParams(1.0, c["dt"], c["eps2"], c["steps"])))
+        want = golden_arrays[c["key"] + "_acc_oracle"]
+        dev = 0.0 if c["n"] == 1 else nb_accel_dev(a, want)
+        tol = F64_ACC_TOL if c["precision"] == "double" else F32_ACC_TOL
+        worst[c["key"]] = dev
+        assert dev <= tol, (c["key"], dev)
+        if c["n"] == 1:
+            assert np.all(a == 0.0)
+    print("accel_dev per golden case:", worst)
+
+
+def test_golden_case_trajectories(golden_cases, golden_arrays, oracle):
+    for c in golden_cases:
+        s = cube(c["n"], c["seed"], c["precision"])
+        p = nb.SimParams(1.0, c["dt"], c["eps2"], c["steps"])
+        fin = nb.simulate(s, p)
+        pos = fin.position_matrix()
+        opos = golden_arrays[c["key"] + "_pos_oracle"]
+        if c["n"] == 1:
+            np.testing.assert_array_equal(pos, golden_arrays[c["key"] + "_pos_ref"])
+            continue
+        dev = oracle.position_dev(pos, opos)
+        if c["precision"] == "double":
+            assert dev <= F64_POS_TOL, (c["key"], dev)
+        else:
+            ref_dev = oracle.position_dev(golden_arrays[c["key"] + "_pos_ref"], opos)
+            assert dev <= max(10 * ref_dev, 1e-7), (c["key"], dev, ref_dev)
+
+
+def nb_accel_dev(got, want):
+    from oracle.oracle import accel_dev
+    return accel_dev(got, want)
+
+
+def test_c1_known_answer(golden_constants, golden_arrays, oracle):
+    """BASELINE.json configs[0]: checksum 9.5618706445328652 (compiled reference)."""
+    cfg = nb.BASELINE_CONFIGS["C1"]
+    s = cfg.system()
+    np.testing.assert_array_equal(s.position_matrix(), golden_arrays["c1_pos0"])
+    a = as_mat(accel_of(s, cfg.params()))
+    assert nb_accel_dev(a, golden_arrays["c1_acc_oracle"]) <= F64_ACC_TOL
+    fin = nb.simulate(s, cfg.params())
+    cs = nb.checksum(fin)
+    want = golden_constants["c1_checksum"]
+    assert abs(cs - want) / abs(want) <= 1e-12, (cs, want)
+    assert oracle.position_dev(fin.position_matrix(), golden_arrays["c1_pos_oracle"]) <= F64_POS_TOL
+    assert oracle.position_dev(fin.position_matrix(), golden_arrays["c1_pos_final"]) <= F64_POS_TOL
+
+
+def test_c1_single_precision_trajectory(golden_arrays, oracle):
+    cfg = nb.BASELINE_CONFIGS["C1"]
+    s = uniform_cube(1024, 0, nb.Precision.SINGLE)
+    fin = nb.simulate(s, cfg.params())
+    opos = golden_arrays["c1_f32_pos_oracle"]
+    ref_dev = oracle.position_dev(golden_arrays["c1_f32_pos_final"], opos)
+    dev = oracle.position_dev(fin.position_matrix(), opos)
+    assert dev <= 10 * ref_dev, (dev, ref_dev)
+
+
+def test_reference_golden_sim_checksum(golden_constants):
+    """GOLDEN_SIM_CHECKSUM (pkg/tests/conftest.py:25-29): N=256, steps=10, seed 42,
+    G=1, dt=0.01, eps2=1e-9, double, within 1e-12."""
+    s = nb.init_system(256, nb.Seed(42))
+    fin = nb.simulate(s, nb.SimParams(1.0, 0.01, 1e-9, 10))
+    want = golden_constants["sim_checksum_n256_seed42_steps10"]
+    assert want == 387.73663935192604
+    assert abs(nb.checksum(fin) - want) / want <= 1e-12
+
+
+# --------------------------------------------------------------------------- update: bit-exact
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_integrate_step_bitwise(prec, oracle):
+    s = cube(1000, 3, prec)
+    acc = accel_of(s, nb.SimParams(1.0, 1e-3, 1e-3, 1))
+    gpu = s.copy()
+    nb.integrate_step(gpu, acc, nb.SimParams(1.0, 1e-3, 1e-3, 1))
+    ref = s.copy()
+    oracle.step_soa(*ref.positions, *ref.velocities, acc.x, acc.y, acc.z, 1e-3)
+    for u, v in zip(gpu.positions + gpu.velocities, ref.positions + ref.velocities):
+        np.testing.assert_array_equal(u, v)
+
+
+def test_integrate_force_free_drift():
+    s = nb.system_from_arrays([[0.0, 0.0, 0.0]], [[0.25, -1.0, 2.0]], [1.0])
+    acc = nb.AccelerationBuffer.allocate(1, nb.Precision.DOUBLE)
+    nb.integrate_step(s, acc, nb.SimParams(dt=0.5, steps=1))
+    assert s.positions[0][0] == 0.125 and s.positions[1][0] == -0.5 and s.positions[2][0] == 1.0
+    assert s.velocities[0][0] == 0.25
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_kick_kernel_bitwise(prec, oracle):
+    import torch
+    dtype = np.dtype(np.float32 if prec == "single" else np.float64)
+    rng = np.random.default_rng(5)
+    n = 777
+    v, a1, a0 = (rng.standard_normal((n, 3)).astype(dtype) for _ in range(3))
+    dev = torch.device("cuda")
+    T = {np.float32: torch.float32, np.float64: torch.float64}[dtype.type]
+    def pk(x):
+        t = torch.zeros((n, 4), dtype=T)
+        t[:, :3] = torch.from_numpy(x)
+        return t.to(dev)
+    tv, t1, t0 = pk(v), pk(a1), pk(a0)
+    sfx = "_f32" if prec == "single" else "_f64"
+    _native.call("nb_dev_kick" + sfx, tv.data_ptr(), t1.data_ptr(), t0.data_ptr(), n, 0.5 * 1e-3, 0)
+    got = tv[:, :3].cpu().numpy()
+    vx, vy, vz = (np.ascontiguousarray(v[:, k]) for k in range(3))
+    oracle.kick(vx, vy, vz, [np.ascontiguousarray(a1[:, k]) for k in range(3)],
+                [np.ascontiguousarray(a0[:, k]) for k in range(3)], 0.5 * 1e-3)
+    np.testing.assert_array_equal(got, np.stack([vx, vy, vz], 1))
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_fused_step_matches_manual_pass_bitwise(prec):
+    """pkg/tests/test_kernels.py:153-166: one-step positions equal a manual
+    compute_accelerations + integrate_step pass, bit for bit (the fused
+    epilogue runs the same rounding sequence as the stand-alone update)."""
+    s = cube(2000, 4, prec)
+    p = nb.SimParams(1.0, 1e-3, 1e-3, 1)
+    manual = s.copy()
+    acc = accel_of(manual, p)
+    nb.integrate_step(manual, acc, p)
+    fin = nb.simulate(s, p)
+    for u, v in zip(fin.positions, manual.positions):
+        np.testing.assert_array_equal(u, v)
+
+
+# --------------------------------------------------------------------------- simulate contract
+
+def test_simulate_leaves_input_untouched():
+    s = nb.init_system(16, nb.Seed(1))
+    before = [c.copy() for c in s.positions]
+    nb.simulate(s, nb.SimParams(1.0, 0.01, 1e-9, 10), nb.reference_variant())
+    for u, v in zip(before, s.positions):
+        assert np.array_equal(u, v)
+
+
+def test_simulate_aos_equals_soa():
+    s = cube(300, 9, "double")
+    p = nb.SimParams(1.0, 1e-3, 1e-3, 4)
+    a = nb.simulate(s, p)
+    b = nb.simulate(nb.convert_layout(s, nb.Layout.AOS), p, nb.KernelVariant(nb.Layout.AOS))
+    assert b.layout is nb.Layout.AOS
+    np.testing.assert_array_equal(a.position_matrix(), b.position_matrix())
+
+
+def test_variant_layout_mismatch_rejected():
+    with pytest.raises(ValueError):
+        nb.simulate(two_body(layout=nb.Layout.AOS), EPS0, nb.reference_variant())
+    with pytest.raises(ValueError):
+        nb.simulate(two_body(), EPS0, nb.KernelVariant(nb.Layout.SOA, block=8))
+
+
+def test_two_body_mirror_symmetry():
+    fin = nb.simulate(two_body(), nb.SimParams(1.0, 0.01, 1e-9, 50), nb.reference_variant())
+    x, y, z = fin.positions
+    np.testing.assert_allclose(x[0] + x[1], 1.0, atol=1e-14)
+    np.testing.assert_allclose(y[0] + y[1], 0.0, atol=1e-14)
+    np.testing.assert_allclose(z[0] + z[1], 0.0, atol=1e-14)
+
+
+def test_momentum_conserved_from_rest():
+    s = nb.init_system(256, nb.Seed(42))
+    fin = nb.simulate(s, nb.SimParams(1.0, 0.01, 1e-9, 100))
+    m = fin.masses
+    v = np.stack(fin.velocities, axis=1)
+    assert np.linalg.norm(m @ v) <= 1e-9 * float(np.sum(m * np.linalg.norm(v, axis=1)))
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_runs_are_bitwise_reproducible(prec):
+    s = cube(20000, 8, prec)
+    p = nb.SimParams(1.0, 1e-3, 1e-3, 3)
+    a = nb.simulate(s, p).position_matrix()
+    b = nb.simulate(s, p).position_matrix()
+    np.testing.assert_array_equal(a, b)
+
+
+def test_native_kernels_launched():
+    before = _native.launch_count()
+    nb.simulate(cube(64, 1, "single"), nb.SimParams(1.0, 1e-3, 1e-3, 2))
+    assert _native.launch_count() - before >= 3
+
+
+# --------------------------------------------------------------------------- sizes & edges
+
+RAGGED = [1, 2, 3, 5, 31, 127, 128, 129, 255, 256, 257, 1023, 1024, 1025, 3001, 5000]
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("n", RAGGED)
+def test_ragged_sizes(prec, n, oracle):
+    s = cube(n, 100 + n, prec)
+    eps2 = 1e-3
+    a = as_mat(accel_of(s, nb.SimParams(1.0, 1e-3, eps2, 1)))
+    pos = s.position_matrix()
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)),
+                                s.masses.astype(np.float64), np.arange(n), 1.0, eps2)
+    if n == 1:
+        assert np.all(a == 0)
+        return
+    tol = F64_ACC_TOL if prec == "double" else F32_ACC_TOL
+    assert nb_accel_dev(a, want) <= tol
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("n", [2, 130, 1025, 4099])
+def test_zero_softening_excludes_self(prec, n, oracle):
+    s = cube(n, 7 * n, prec)
+    a = as_mat(accel_of(s, nb.SimParams(1.0, 1e-3, 0.0, 1)))
+    pos = s.position_matrix()
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)),
+                                s.masses.astype(np.float64), np.arange(n), 1.0, 0.0)
+    assert np.all(np.isfinite(a))
+    tol = 1e-11 if prec == "double" else 1e-4  # unsoftened: condition number is unbounded
+    assert nb_accel_dev(a, want) <= tol
+
+
+@pytest.mark.parametrize("cfg_name", ["C2", "C3-f32", "C3-f64", "C4"])
+def test_full_size_accelerations_row_sampled(cfg_name, oracle):
+    """BASELINE sizes: 192 rows (first, last, random) of the initial accelerations
+    against the long-double oracle."""
+    cfg = nb.BASELINE_CONFIGS[cfg_name]
+    s = cfg.system()
+    a = as_mat(accel_of(s, cfg.params()))
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([[0, 1, cfg.n - 1], rng.integers(0, cfg.n, 189)]))
+    pos = s.position_matrix()
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)),
+                                s.masses.astype(np.float64), rows, 1.0, cfg.softening_sq)
+    tol = F64_ACC_TOL if cfg.precision is nb.Precision.DOUBLE else F32_ACC_TOL
+    dev = nb_accel_dev(a[rows], want)
+    print(cfg_name, "accel_dev", dev)
+    assert dev <= tol
+
+
+def test_plummer_row_sampled(oracle):
+    """C5's distribution (Plummer, equal masses) at 1/16 of its N."""
+    s = nb.plummer_sphere(262144, 0, nb.Precision.SINGLE)
+    a = as_mat(accel_of(s, nb.SimParams(1.0, 1e-4, 1e-4, 1)))
+    rows = np.random.default_rng(2).integers(0, 262144, 64)
+    pos = s.position_matrix()
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)),
+                                s.masses.astype(np.float64), rows, 1.0, 1e-4)
+    assert nb_accel_dev(a[rows], want) <= F32_ACC_TOL
+
+
+def test_full_size_trajectory_properties():
+    """C3-f32 at full size: finite, deterministic, and momentum stays at the
+    rounding level of its initial value (a size-independent property)."""
+    cfg = nb.BASELINE_CONFIGS["C3-f32"]
+    s = cfg.system()
+    fin = nb.simulate(s, cfg.params())
+    v = np.stack(fin.velocities, 1).astype(np.float64)
+    v0 = np.stack(s.velocities, 1).astype(np.float64)
+    m = fin.masses.astype(np.float64)
+    assert np.all(np.isfinite(v)) and np.all(np.isfinite(fin.position_matrix()))
+    p0, p1 = m @ v0, m @ v
+    scale = float(np.sum(m * np.linalg.norm(v, axis=1)))
+    assert np.linalg.norm(p1 - p0) <= 1e-5 * scale
+
+
+# --------------------------------------------------------------------------- sharding on one GPU
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_sharded_driver_on_one_gpu(prec, world):
+    """The multi-GPU step loop with P emulated ranks on one device, run in lock
+    step (no rank waits on another's kernel): every rank owns an i-shard, sums
+    its local sources into the FP64 carry, then the rest; positions are
+    exchanged by copying rows (the all-gather)."""
+    from paper_2203_08263_b200.device import DeviceState, needs_self_mask
+    from paper_2203_08263_b200.sharded import pad_system, shard_range
+    from paper_2203_08263_b200._native import NB_STEP_FIRST, NB_STEP_KICK_DRIFT, NB_STEP_FINAL_KICK
+    s = cube(3000, 21, prec)
+    p = nb.SimParams(1.0, 1e-3, 1e-3, 4)
+    ref = nb.simulate(s, p)
+    dtype = s.precision.dtype
+    pos, vel, m = pad_system(s.position_matrix().astype(dtype), np.stack(s.velocities, 1), s.masses, world)
+    npad = pos.shape[0]
+    ranks = []
+    for r in range(world):
+        i0, ni = shard_range(npad, r, world)
+        ranks.append(DeviceState(pos, vel, m, dtype, i_begin=i0, n_i=ni))
+    mask = needs_self_mask(m[: s.count], p.softening_sq, dtype)
+    for step in range(p.steps + 1):
+        mode = NB_STEP_FIRST if step == 0 else (NB_STEP_KICK_DRIFT if step < p.steps else NB_STEP_FINAL_KICK)
+        for st in ranks:
+            st.step(1.0, p.softening_sq, p.dt, mode, mask, j_begin=st.i_begin, j_count=st.n_i, carry_mode=1)
+            st.step(1.0, p.softening_sq, p.dt, mode, mask, j_begin=(st.i_begin + st.n_i) % npad,
+                    j_count=npad - st.n_i, carry_mode=2)
+        if mode != NB_STEP_FINAL_KICK:
+            for st in ranks:
+                st.swap()
+            for st in ranks:
+                for src in ranks:
+                    sl = slice(src.i_begin, src.i_begin + src.n_i)
+                    st.pos_cur[sl] = src.pos_cur[sl]
+    got = ranks[0].pos_cur[: s.count, :3].cpu().numpy().astype(np.float64)
+    tol = 1e-13 if prec == "double" else 1e-6
+    from oracle.oracle import position_dev
+    assert position_dev(got, ref.position_matrix()) <= tol
+
+
+# --------------------------------------------------------------------------- plugin + diagnostics
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_backend_plugin_protocol(prec, oracle):
+    from paper_2203_08263_b200 import backend
+    s = cube(513, 17, prec)
+    px, py, pz = (c.copy() for c in s.positions)
+    ax, ay, az = (np.zeros(513, s.precision.dtype) for _ in range(3))
+    backend.accel_soa(px, py, pz, s.masses, 1.0, 1e-3, True, 0, 1, ax, ay, az)
+    want = oracle.accel_rows_ld(px, py, pz, s.masses.astype(np.float64), np.arange(513), 1.0, 1e-3)
+    tol = F64_ACC_TOL if prec == "double" else F32_ACC_TOL
+    assert nb_accel_dev(np.stack([ax, ay, az], 1), want) <= tol
+    pos = np.ascontiguousarray(np.stack([px, py, pz], 1))
+    bx, by, bz = (np.zeros_like(ax) for _ in range(3))
+    backend.accel_aos(pos, s.masses, 1.0, 1e-3, bx, by, bz)
+    np.testing.assert_array_equal(np.stack([ax, ay, az], 1), np.stack([bx, by, bz], 1))
+    vx, vy, vz = (c.copy() for c in s.velocities)
+    rpx, rpy, rpz, rvx, rvy, rvz = (c.copy() for c in (px, py, pz, vx, vy, vz))
+    backend.step_soa(px, py, pz, vx, vy, vz, ax, ay, az, 1e-3, 4)
+    oracle.step_soa(rpx, rpy, rpz, rvx, rvy, rvz, ax, ay, az, 1e-3)
+    for u, v in zip((px, py, pz, vx, vy, vz), (rpx, rpy, rpz, rvx, rvy, rvz)):
+        np.testing.assert_array_equal(u, v)
+
+
+def test_backend_simulate_matches_package():
+    from paper_2203_08263_b200 import backend
+    s = cube(700, 5, "double")
+    p = nb.SimParams(1.0, 1e-3, 1e-3, 3)
+    cols = [c.copy() for c in s.positions + s.velocities]
+    backend.simulate_soa(*cols, s.masses, 1.0, 1e-3, 1e-3, 3)
+    np.testing.assert_array_equal(np.stack(cols[:3], 1), nb.simulate(s, p).position_matrix())
+
+
+def test_energy_diagnostics(oracle):
+    s = cube(2048, 31, "double")
+    p = nb.SimParams(1.0, 1e-3, 1e-3, 1)
+    d = nb.diagnostics_gpu(s, p)
+    want = oracle.diagnostics(s.position_matrix(), np.stack(s.velocities, 1), s.masses, 1.0, 1e-3)
+    assert abs(d["kinetic"] - want["kinetic"]) <= 1e-12 * abs(want["kinetic"])
+    assert abs(d["potential"] - want["potential"]) <= 1e-12 * abs(want["potential"])
+    np.testing.assert_allclose(d["momentum"], want["momentum"], rtol=1e-12, atol=1e-13)
