@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 all-pairs N-body hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3-f32] [--impl ours|reference]
+
+One bench *step* = one ``simulate`` of the configuration (``steps`` velocity-
+Verlet steps = steps+1 force evaluations of N^2 interactions each, the loop of
+kernels/__init__.py:240-252) on the device-resident initial state.  Rank 0
+prints ONE JSON line.
+
+* ``value``  -- interactions/s over the whole job (all ranks), inputs resident
+  in HBM, CUDA events around each step on the launching stream, max over ranks;
+  L2 is flushed (256 MB write) between timed steps, outside the events.
+* ``e2e``    -- the same metric through the public API ``simulate(system, params)``
+  from host NumPy arrays (pinned staging, H2D, kernels, D2H) every step.
+* ``roofline`` -- the fused force+update kernel: 20 flop/interaction x N^2 per
+  launch / mean launch time, against the nominal FP32 (FP64) CUDA-core peak
+  148 SM x 128 (64) lanes x 2 x 1.965 GHz (MEASURED_PEAKS.json carries no
+  CUDA-core figure; the microbenchmarked FFMA peak is reported beside it).
+* ``cpu_baseline`` -- the reference's own compiled kernel (oracle/_ref, built
+  from /root/reference by oracle/Makefile) on all host cores, rank 0 at N=1.
+
+``--impl reference`` times only the reference's CPU implementation of the path
+(same config, metric and unit) and prints its own line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "body-body interactions/s (GFLOP/s at 20 flop/int) vs FP32/FP64 CUDA-core peak"
+UNIT = "interactions/s"
+FLOP_PER_INTERACTION = 20
+NOMINAL_CLOCK_HZ = 1.965e9
+SMS = 148
+# Measured on this pool's B200 with tools/pipe_peaks.cu (profiles/pipe_peaks_r01.txt):
+# FFMA 121.3 and DFMA 60.2 lane-ops/SM/clk at 1965 MHz.
+MEASURED_FFMA_TFLOPS = 70.6
+MEASURED_DFMA_TFLOPS = 35.0
+PUBLISHED_CPU_GFLOPS_FP32 = 1524.0  # PAPER.md:445, Numba FP32 best, reference convention
+L2_FLUSH_BYTES = 256 << 20
+
+
+def nominal_peak_tflops(precision_bytes: int) -> float:
+    lanes = 128 if precision_bytes == 4 else 64
+    return SMS * lanes * 2 * NOMINAL_CLOCK_HZ / 1e12
+
+
+# --------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:  # pragma: no cover
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        loaded = [s for s, p in zip(sm, power) if p > 300] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+# --------------------------------------------------------------------------- CPU baseline
+
+def cpu_reference_rate(cfg, sys0, budget_s: float = 20.0, fixed_n: int = 0):
+    """Reference CPU path on this host: the reference's compiled accel_soa
+    (oracle/_ref) over all host threads, soa-recip (its fastest rung), on the
+    config's state.  Returns (interactions/s, description dict)."""
+    from oracle import oracle as O
+    threads = O.host_threads()
+    dtype = cfg.precision.dtype
+    n = fixed_n or cfg.n
+    cols = [np.ascontiguousarray(c[:n], dtype=dtype) for c in sys0.positions]
+    m = np.ascontiguousarray(sys0.masses[:n], dtype=dtype)
+    out = [np.empty(n, dtype) for _ in range(3)]
+    if O.ref_available():
+        R = O.ref_module()
+        kind = "reference"
+
+        def run():
+            R.accel_soa(cols[0], cols[1], cols[2], m, 1.0, cfg.softening_sq, True, 0, threads, *out)
+    else:  # the restated port (oracle/nbody_oracle.c), same arithmetic
+        kind = "port"
+
+        def run():
+            O.accel_soa(cols[0], cols[1], cols[2], m, 1.0, cfg.softening_sq, True, 0, threads)
+    t0 = time.perf_counter()
+    run()
+    t = time.perf_counter() - t0
+    return float(n) * n / t, {"kind": kind, "cores": threads, "seconds": t, "n": n}
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def load_traffic(config_name: str):
+    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            data = json.load(f)
+        entry = data.get(config_name) or {}
+        return entry.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def run_ours(args) -> dict:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2203_08263_b200 as nb
+    from paper_2203_08263_b200 import _native
+    from paper_2203_08263_b200._native import NB_STEP_FINAL_KICK, NB_STEP_FIRST, NB_STEP_KICK_DRIFT
+    from paper_2203_08263_b200.device import DeviceState, needs_self_mask
+    from paper_2203_08263_b200.sharded import pad_system, run_sharded, shard_range
+
+    world, rank, local = _dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = nb.BASELINE_CONFIGS[args.config]
+    params = cfg.params()
+    sys0 = cfg.system()
+    dtype = cfg.precision.dtype
+    pbytes = dtype.itemsize
+    pos0 = sys0.position_matrix().astype(dtype)
+    vel0 = np.stack(sys0.velocities, axis=1)
+    m0 = sys0.masses
+    pos, vel, m = pad_system(pos0, vel0, m0, world)
+    npad = pos.shape[0]
+    i0, ni = shard_range(npad, rank, world)
+    mask = needs_self_mask(m0, cfg.softening_sq, dtype)
+    state = DeviceState(pos, vel, m, dtype, device=dev, i_begin=i0, n_i=ni)
+    pristine_pos = state.pos_a.clone()
+    pristine_vel = state.vel.clone()
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    g, dt, eps2, steps = params.gravitational_constant, params.dt, params.softening_sq, params.steps
+
+    def reset():
+        state.pos_a.copy_(pristine_pos)
+        state.vel.copy_(pristine_vel)
+        state.acc.zero_()
+        state.cur_is_a = True
+
+    launch_events = []
+
+    def one_step(record_launches: bool):
+        """One simulate of the config on the resident state (steps+1 launches)."""
+        if world == 1:
+            evs = [torch.cuda.Event(enable_timing=True)] if record_launches else None
+            if evs:
+                evs[0].record()
+            for s in range(steps + 1):
+                mode = NB_STEP_FIRST if s == 0 else (NB_STEP_KICK_DRIFT if s < steps else NB_STEP_FINAL_KICK)
+                state.step(g, eps2, dt, mode, mask)
+                if mode != NB_STEP_FINAL_KICK:
+                    state.swap()
+                if evs is not None:
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record()
+                    evs.append(e)
+            if evs is not None:
+                launch_events.append(evs)
+        else:
+            def gather(full, local_rows):
+                return dist.all_gather_into_tensor(full, local_rows, async_op=True)
+            run_sharded(state, g, dt, eps2, steps, mask, gather, world)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    # ---------------------------------------------------------------- warm-up
+    for _ in range(args.warmup):
+        reset()
+        one_step(False)
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- timed region
+    clocks = ClockSampler(local)
+    clocks.start()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches_before = _native.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        reset()
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        starts[k].record()
+        one_step(record_launches=(world == 1))
+        ends[k].record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = _native.launch_count() - launches_before
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_s = sum(step_ms) / 1e3
+    if world > 1:
+        t = torch.tensor([total_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+    interactions = float(cfg.n) * cfg.n * (steps + 1) * args.steps
+    value = interactions / total_s
+
+    # per-launch kernel durations (N=1): the dominant (only) kernel of the step
+    kernel_ms = []
+    for evs in launch_events:
+        kernel_ms += [a.elapsed_time(b) for a, b in zip(evs[:-1], evs[1:])]
+    peak = nominal_peak_tflops(pbytes)
+    if kernel_ms:
+        mean_launch_s = statistics.mean(kernel_ms) / 1e3
+        achieved = FLOP_PER_INTERACTION * float(cfg.n) * cfg.n / mean_launch_s / 1e12
+    else:
+        mean_launch_s = total_s / (args.steps * (steps + 1))
+        achieved = FLOP_PER_INTERACTION * interactions / total_s / 1e12 / world
+    roofline = {
+        "bound": "fp32_cuda_core" if pbytes == 4 else "fp64_cuda_core",
+        "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+        "peak_source": "nominal 148 SM x %d lanes x 2 x 1.965 GHz (no CUDA-core figure in MEASURED_PEAKS.json)"
+                       % (128 if pbytes == 4 else 64),
+        "peak_measured_microbench": MEASURED_FFMA_TFLOPS if pbytes == 4 else MEASURED_DFMA_TFLOPS,
+        "frac_of_measured_microbench": achieved / (MEASURED_FFMA_TFLOPS if pbytes == 4 else MEASURED_DFMA_TFLOPS),
+        "kernel": "nb::step_kernel (fused force + velocity-Verlet epilogue)",
+        "mean_launch_ms": mean_launch_s * 1e3,
+        "algorithmic_flop_per_launch": FLOP_PER_INTERACTION * float(cfg.n) * cfg.n,
+        "traffic": load_traffic(args.config),
+    }
+
+    # ---------------------------------------------------------------- e2e through the public API
+    e2e = None
+    if not args.no_e2e:
+        sys_host = cfg.system()
+        for _ in range(min(args.warmup, 2)):
+            nb.simulate(sys_host, params)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        final = None
+        for _ in range(args.steps):
+            final = nb.simulate(sys_host, params)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": interactions / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * npad * 4 * pbytes,
+               "d2h_bytes_per_step": 2 * cfg.n * 3 * pbytes,
+               "api": "paper_2203_08263_b200.simulate(ParticleSystem, SimParams) from host NumPy arrays",
+               "checksum": nb.checksum(final)}
+
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_s * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": (FLOP_PER_INTERACTION * float(cfg.n) * cfg.n * steps * args.steps / total_s / 1e9)
+                       / PUBLISHED_CPU_GFLOPS_FP32 if pbytes == 4 else None,
+        "dtype": "f32" if pbytes == 4 else "f64", "data": "synthetic (BASELINE.json generator, seed 0)",
+        "config": {"workload": cfg.name, "n_bodies": cfg.n, "integrator_steps": steps,
+                   "force_evaluations_per_step": steps + 1, "softening_sq": cfg.softening_sq,
+                   "dt": cfg.dt, "distribution": cfg.generator.__name__,
+                   "parallelism": f"i-shard x{world}" if world > 1 else "1 GPU",
+                   "l2": "flushed (256 MB write) between timed steps"},
+        "gflops_20": FLOP_PER_INTERACTION * value / 1e9,
+        "gflops_reference_convention": FLOP_PER_INTERACTION * float(cfg.n) * cfg.n * steps * args.steps
+                                       / total_s / 1e9,
+        "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        rate, desc = cpu_reference_rate(cfg, sys0)
+        result["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": desc["cores"], "kind": desc["kind"],
+            "sample": f"one force evaluation (N^2 = {desc['n'] ** 2:.3e} interactions) of the "
+                      f"{cfg.name} initial state through the reference's compiled accel_soa "
+                      f"(soa-recip, {desc['cores']} threads), {desc['seconds']:.2f} s"}
+    if world > 1:
+        dist.destroy_process_group()
+    return result if rank == 0 else None
+
+
+def run_reference(args) -> dict:
+    """The reference's own CPU implementation of the path (oracle/_ref) on the
+    host cores; same config, metric and unit.  Rank 0 only."""
+    import paper_2203_08263_b200 as nb
+    from oracle import oracle as O
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return None
+    cfg = nb.BASELINE_CONFIGS[args.config]
+    sys0 = cfg.system()
+    # size the per-step sample so the whole run stays within ~3 minutes
+    rate, desc = cpu_reference_rate(cfg, sys0)
+    budget = 150.0
+    per_step = desc["seconds"]
+    n_s = cfg.n
+    if per_step * (args.steps + args.warmup) > budget:
+        n_s = int(cfg.n * (budget / (per_step * (args.steps + args.warmup))) ** 0.5) // 1024 * 1024
+        n_s = max(n_s, 4096)
+    for _ in range(args.warmup):
+        cpu_reference_rate(cfg, sys0, fixed_n=n_s)
+    total, inter = 0.0, 0.0
+    for _ in range(args.steps):
+        r, d = cpu_reference_rate(cfg, sys0, fixed_n=n_s)
+        total += d["seconds"]
+        inter += float(n_s) * n_s
+    value = inter / total
+    sample = (f"per step one force evaluation of the first {n_s} bodies of the {cfg.name} state "
+              f"({float(n_s) ** 2:.3e} interactions) through the reference's compiled accel_soa "
+              f"(soa-recip, {desc['cores']} threads); simulate() is steps+1 such evaluations")
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32" if cfg.precision.dtype.itemsize == 4 else "f64",
+        "data": "synthetic (BASELINE.json generator, seed 0)",
+        "config": {"workload": cfg.name, "n_bodies": cfg.n, "sample_bodies": n_s},
+        "gflops_20": FLOP_PER_INTERACTION * value / 1e9,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": desc["cores"], "kind": desc["kind"],
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3-f32",
+                    choices=["C1", "C2", "C3-f32", "C3-f64", "C4", "C5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
