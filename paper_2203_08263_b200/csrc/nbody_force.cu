@@ -29,6 +29,47 @@
 #include "nbody_common.cuh"
 #include "nbody_kernels.h"
 
+#include <cstdlib>
+
+// Tuning knobs (overridable with -D for variant sweeps, tools/variants.py).
+#ifndef NB_F32_K
+#define NB_F32_K 6
+#endif
+#ifndef NB_F32_T
+#define NB_F32_T 128
+#endif
+#ifndef NB_F32_TJ
+#define NB_F32_TJ 256
+#endif
+#ifndef NB_F32_MINB
+#define NB_F32_MINB 3
+#endif
+#ifndef NB_F32_UNROLL
+#define NB_F32_UNROLL 4
+#endif
+#ifndef NB_F32_PIPE
+#define NB_F32_PIPE 0
+#endif
+#ifndef NB_CHUNK
+#define NB_CHUNK 32
+#endif
+#ifndef NB_F64_K
+#define NB_F64_K 4
+#endif
+#ifndef NB_F64_T
+#define NB_F64_T 128
+#endif
+#ifndef NB_F64_TJ
+#define NB_F64_TJ 128
+#endif
+#ifndef NB_F64_MINB
+#define NB_F64_MINB 3
+#endif
+#ifndef NB_F64_UNROLL
+#define NB_F64_UNROLL 4
+#endif
+
+
 namespace nb {
 
 struct Sched {
@@ -75,7 +116,7 @@ __device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
 // K target bodies per thread as K/2 packed pairs.  The FP64 segment sums live in
 // shared memory (3*K doubles per thread, touched once per tile) so the inner
 // loop keeps its registers for the pairs and their temporaries.
-template <int K_, bool MASK>
+template <int K_, bool MASK, int UNROLL_>
 struct CoreF32 {
   using R = float;
   static constexpr int K = K_;
@@ -139,6 +180,69 @@ struct CoreF32 {
       tz[q] = fma2(dz, w, tz[q]);
     }
   }
+  // Stage A of a source body: separations, d2 and the MUFU.RSQ pair.
+  __device__ __forceinline__ void stage_a(const F4& pj, f2x* dx, f2x* dy, f2x* dz, f2x* r) const {
+    const f2x xj = pk(pj.x, pj.x), yj = pk(pj.y, pj.y), zj = pk(pj.z, pj.z);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      dx[q] = add2(xj, nx[q]);
+      dy[q] = add2(yj, ny[q]);
+      dz[q] = add2(zj, nz[q]);
+      f2x d2 = fma2(dx[q], dx[q], e2);
+      d2 = fma2(dy[q], dy[q], d2);
+      d2 = fma2(dz[q], dz[q], d2);
+      float d2a, d2b;
+      upk(d2, d2a, d2b);
+      r[q] = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
+    }
+  }
+  // Stage B: w = m r^3 and the accumulation.
+  __device__ __forceinline__ void stage_b(float m, int jj, const f2x* dx, const f2x* dy, const f2x* dz,
+                                          const f2x* r) {
+    const f2x mj = pk(m, m);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const f2x r2 = mul2(r[q], r[q]);
+      const f2x mr = mul2(r[q], mj);
+      f2x w = mul2(mr, r2);
+      if (MASK) {
+        float wa, wb;
+        upk(w, wa, wb);
+        if (jj == selfj[2 * q]) wa = 0.f;
+        if (jj == selfj[2 * q + 1]) wb = 0.f;
+        w = pk(wa, wb);
+      }
+      tx[q] = fma2(dx[q], w, tx[q]);
+      ty[q] = fma2(dy[q], w, ty[q]);
+      tz[q] = fma2(dz[q], w, tz[q]);
+    }
+  }
+  // A full tile, software-pipelined by one source body: stage A of body j+1
+  // (whose MUFUs have a whole stage of independent FP32 work to hide behind)
+  // is interleaved with stage B of body j.
+  template <int TJ>
+  __device__ __forceinline__ void full_tile(const F4* tb) {
+#if NB_F32_PIPE
+    f2x dx[KP], dy[KP], dz[KP], r[KP];
+    F4 p = tb[0];
+    stage_a(p, dx, dy, dz, r);
+    float m = p.w;
+#pragma unroll UNROLL_
+    for (int jj = 1; jj < TJ; ++jj) {
+      const F4 q = tb[jj];
+      f2x dx1[KP], dy1[KP], dz1[KP], r1[KP];
+      stage_a(q, dx1, dy1, dz1, r1);
+      stage_b(m, jj - 1, dx, dy, dz, r);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) { dx[k] = dx1[k]; dy[k] = dy1[k]; dz[k] = dz1[k]; r[k] = r1[k]; }
+      m = q.w;
+    }
+    stage_b(m, TJ - 1, dx, dy, dz, r);
+#else
+#pragma unroll UNROLL_
+    for (int jj = 0; jj < TJ; ++jj) interact(tb[jj], jj);
+#endif
+  }
   __device__ __forceinline__ void end_tile() {
 #pragma unroll
     for (int q = 0; q < KP; ++q) {
@@ -157,7 +261,7 @@ struct CoreF32 {
 };
 
 // ---------------------------------------------------------------- FP64 core
-template <int K_, bool MASK>
+template <int K_, bool MASK, int UNROLL_>
 struct CoreF64 {
   using R = double;
   static constexpr int K = K_;
@@ -182,6 +286,11 @@ struct CoreF64 {
   }
   __device__ __forceinline__ void begin_tile() {}
   __device__ __forceinline__ void end_tile() {}
+  template <int TJ>
+  __device__ __forceinline__ void full_tile(const D4* tb) {
+#pragma unroll UNROLL_
+    for (int jj = 0; jj < TJ; ++jj) interact(tb[jj], jj);
+  }
   __device__ __forceinline__ void interact(const D4& pj, int jj) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -249,7 +358,7 @@ __device__ __forceinline__ void finalize_body(const StepArgs<R>& a, int64_t il, 
 }
 
 // ---------------------------------------------------------------- stream-K kernel
-template <class Core, int T, int TJ, int MINB>
+template <class Core, int T, int TJ, int MINB, int CH>
 __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename Core::R> a) {
   using R = typename Core::R;
   using B = V4<R>;
@@ -257,15 +366,19 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
   constexpr int IB = T * K;
   constexpr int PER = TJ / T;  // tile elements staged per thread
   static_assert(TJ % T == 0, "tile must be a multiple of the block");
+  static_assert(TJ % CH == 0, "tile must be a multiple of the stream-K chunk");
 
   __shared__ B tile[2][TJ];
   __shared__ double s_sums[Core::SMEM_SUMS * T];
-  __shared__ int s_last;
 
+  // Programmatic dependent launch: wait for the previous kernel in the stream
+  // (positions it wrote), then let the fixup kernel be scheduled as our CTAs drain.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x;
   const int64_t c = blockIdx.x;
   const Sched S{a.units, a.grid};
-  const int64_t NT = a.n_tiles;
+  const int64_t NT = a.n_tiles;  // source chunks of CH bodies per i-block
   const int64_t u_begin = S.start(c), u_end = S.start(c + 1);
 
   Core core;
@@ -275,6 +388,8 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
     const int64_t b = u / NT;
     const int64_t t0 = u - b * NT;
     const int64_t t1 = min(NT, t0 + (u_end - u));
+    // this segment's source offsets [s0, s1) within the j range
+    const int64_t s0 = t0 * CH, s1 = min(t1 * CH, a.j_count);
 
 #pragma unroll
     for (int q = 0; q < K / 2; ++q) {
@@ -285,11 +400,11 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
     core.zero_sums();
 
     B stage[PER];
-    auto load_tile = [&](int64_t t) {
+    auto load_tile = [&](int64_t lo) {
 #pragma unroll
       for (int r = 0; r < PER; ++r) {
-        const int64_t off = t * TJ + r * T + tid;
-        if (off < a.j_count) {
+        const int64_t off = lo + r * T + tid;
+        if (off < s1) {
           int64_t jg = a.j_begin + off;
           if (jg >= a.n_all) jg -= a.n_all;
           stage[r] = ld4(a.pos + jg);
@@ -303,17 +418,17 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
       for (int r = 0; r < PER; ++r) tile[buf][r * T + tid] = stage[r];
     };
 
-    load_tile(t0);
+    load_tile(s0);
     store_tile(0);
     __syncthreads();
 
-    for (int64_t t = t0; t < t1; ++t) {
-      const int buf = (int)((t - t0) & 1);
-      if (t + 1 < t1) load_tile(t + 1);
-      const int64_t off0 = t * TJ;
-      const int count = (int)max((int64_t)0, min((int64_t)TJ, a.j_count - off0));
+    int buf = 0;
+    for (int64_t lo = s0; lo < s1; lo += TJ) {
+      const bool more = lo + TJ < s1;
+      if (more) load_tile(lo + TJ);
+      const int count = (int)min((int64_t)TJ, s1 - lo);
       if (Core::MASK_SELF) {
-        int64_t base = a.j_begin + off0;
+        int64_t base = a.j_begin + lo;
         if (base >= a.n_all) base -= a.n_all;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -325,14 +440,22 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
       core.begin_tile();
       const B* tb = tile[buf];
       if (count == TJ) {
-#pragma unroll 4
-        for (int jj = 0; jj < TJ; ++jj) core.interact(tb[jj], jj);
+        core.template full_tile<TJ>(tb);
       } else {
+        int jj = 0;
 #pragma unroll 1
-        for (int jj = 0; jj < count; ++jj) core.interact(tb[jj], jj);
+        for (; jj + 4 <= count; jj += 4) {
+          core.interact(tb[jj], jj);
+          core.interact(tb[jj + 1], jj + 1);
+          core.interact(tb[jj + 2], jj + 2);
+          core.interact(tb[jj + 3], jj + 3);
+        }
+#pragma unroll 1
+        for (; jj < count; ++jj) core.interact(tb[jj], jj);
       }
       core.end_tile();
-      if (t + 1 < t1) store_tile(buf ^ 1);
+      if (more) store_tile(buf ^ 1);
+      buf ^= 1;
       __syncthreads();
     }
 
@@ -344,8 +467,9 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
         if (il < a.n_i) finalize_body<R>(a, il, core.sum(0, k), core.sum(1, k), core.sum(2, k));
       }
     } else {
-      // Split i-block: publish FP64 partials; the last CTA in combines them in
-      // ascending CTA order (deterministic) and runs the epilogue.
+      // Split i-block: publish this segment's FP64 partial sums; fixup_kernel
+      // (stream-ordered after this launch) combines the contributors of the
+      // i-block in ascending CTA order -- deterministic -- and runs the epilogue.
       const int64_t slot = (u == u_begin) ? 2 * c : 2 * c + 1;
       double* sp = a.slots + slot * 3 * IB;
 #pragma unroll
@@ -354,60 +478,62 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
         sp[IB + k * T + tid] = core.sum(1, k);
         sp[2 * IB + k * T + tid] = core.sum(2, k);
       }
-      __threadfence();
-      __syncthreads();
-      const int64_t cf = S.cta_of(b * NT), cl = S.cta_of(b * NT + NT - 1);
-      if (tid == 0) {
-        const unsigned prev = atomicAdd(a.counters + b, 1u);
-        const int last = prev == (unsigned)(cl - cf);
-        if (last) a.counters[b] = 0u;  // leave the workspace zeroed for the next launch
-        s_last = last;
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        core.zero_sums();
-        for (int64_t cc = cf; cc <= cl; ++cc) {
-          const int64_t sl = (S.start(cc) / NT == b) ? 2 * cc : 2 * cc + 1;
-          const double* q = a.slots + sl * 3 * IB;
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            core.set_sum(0, k, core.sum(0, k) + __ldcg(q + k * T + tid));
-            core.set_sum(1, k, core.sum(1, k) + __ldcg(q + IB + k * T + tid));
-            core.set_sum(2, k, core.sum(2, k) + __ldcg(q + 2 * IB + k * T + tid));
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int64_t il = b * IB + k * T + tid;
-          if (il < a.n_i) finalize_body<R>(a, il, core.sum(0, k), core.sum(1, k), core.sum(2, k));
-        }
-      }
     }
     u += t1 - t0;
   }
 }
 
+// ---------------------------------------------------------------- split i-block fixup
+// One thread per target body of a split i-block: sum the FP64 partials of the
+// contributing CTAs cf..cl in ascending order (slot 2c holds a CTA's first
+// segment, 2c+1 its last) and run the epilogue.  Bodies of i-blocks one CTA
+// covered whole were finished by step_kernel and are skipped.
+template <typename R, int IB>
+__global__ void __launch_bounds__(256) fixup_kernel(const StepArgs<R> a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int64_t il = blockIdx.x * 256LL + threadIdx.x;
+  if (il >= a.n_i) return;
+  const Sched S{a.units, a.grid};
+  const int64_t NT = a.n_tiles;
+  const int64_t b = il / IB, o = il - b * IB;
+  const int64_t cf = S.cta_of(b * NT), cl = S.cta_of(b * NT + NT - 1);
+  if (cf == cl) return;
+  int64_t sl = (S.start(cf) == b * NT) ? 2 * cf : 2 * cf + 1;
+  double tx = 0.0, ty = 0.0, tz = 0.0;
+  for (int64_t cc = cf; cc <= cl; ++cc, sl = 2 * cc) {
+    const double* q = a.slots + sl * 3 * IB + o;
+    tx += q[0];
+    ty += q[IB];
+    tz += q[2 * IB];
+  }
+  finalize_body<R>(a, il, tx, ty, tz);
+}
+
 // ---------------------------------------------------------------- configurations
 // FP32: 128 threads x 8 bodies (4 FFMA2 pairs) = 1024-body i-blocks, 256-body tiles.
 // FP64: 128 threads x 4 bodies = 512-body i-blocks, 128-body tiles.
-template <bool M> struct CoreF32M : CoreF32<8, M> { static constexpr bool MASK_SELF = M; };
-template <bool M> struct CoreF64M : CoreF64<4, M> { static constexpr bool MASK_SELF = M; };
+template <bool M> struct CoreF32M : CoreF32<NB_F32_K, M, NB_F32_UNROLL> {
+  static constexpr bool MASK_SELF = M;
+};
+template <bool M> struct CoreF64M : CoreF64<NB_F64_K, M, NB_F64_UNROLL> {
+  static constexpr bool MASK_SELF = M;
+};
 
 template <typename R> struct Cfg;
 template <> struct Cfg<float> {
-  static constexpr int T = 128, TJ = 256, MINB = 3;
+  static constexpr int T = NB_F32_T, TJ = NB_F32_TJ, MINB = NB_F32_MINB;
   template <bool M> using Core = CoreF32M<M>;
 };
 template <> struct Cfg<double> {
-  static constexpr int T = 128, TJ = 128, MINB = 3;
+  static constexpr int T = NB_F64_T, TJ = NB_F64_TJ, MINB = NB_F64_MINB;
   template <bool M> using Core = CoreF64M<M>;
 };
 
 template <typename R, bool M>
 static const void* kernel_ptr() {
   using C = Cfg<R>;
-  return reinterpret_cast<const void*>(&step_kernel<typename C::template Core<M>, C::T, C::TJ, C::MINB>);
+  return reinterpret_cast<const void*>(&step_kernel<typename C::template Core<M>, C::T, C::TJ, C::MINB, NB_CHUNK>);
 }
 
 template <typename R>
@@ -418,7 +544,7 @@ StepGeometry step_geometry(int64_t n_i, int64_t j_count) {
   g.i_block = C::T * C::template Core<false>::K;
   g.tile = C::TJ;
   g.n_iblocks = (n_i + g.i_block - 1) / g.i_block;
-  g.n_tiles = j_count > 0 ? (j_count + C::TJ - 1) / C::TJ : 1;
+  g.n_tiles = j_count > 0 ? (j_count + NB_CHUNK - 1) / NB_CHUNK : 1;  // stream-K chunks
   g.units = g.n_iblocks * g.n_tiles;
   return g;
 }
@@ -439,8 +565,18 @@ int max_grid() {
     if (per_sm < 1) per_sm = 1;
     best = best > sms * per_sm ? best : sms * per_sm;
   }
+  // Experiment hook: NB_GRID_OVERRIDE=<ctas> replaces the persistent grid size.
+  if (const char* env = getenv("NB_GRID_OVERRIDE")) {
+    const int v = atoi(env);
+    if (v > 0) best = v;
+  }
   cached[dev] = best;
   return best;
+}
+
+// Host mirror of Sched::cta_of.
+static inline int64_t host_cta_of(int64_t u, int64_t grid, int64_t units) {
+  return ((u + 1) * grid + units - 1) / units - 1;
 }
 
 template <typename R>
@@ -453,18 +589,43 @@ cudaError_t launch_step(StepArgs<R> a, bool mask_self, cudaStream_t stream) {
   if ((int64_t)grid > g.units) grid = (int)g.units;
   a.grid = grid;
   using C = Cfg<R>;
+  constexpr int IB = C::T * C::template Core<false>::K;
+
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(C::T);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
   if (mask_self)
-    step_kernel<typename C::template Core<true>, C::T, C::TJ, C::MINB><<<grid, C::T, 0, stream>>>(a);
+    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<true>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
   else
-    step_kernel<typename C::template Core<false>, C::T, C::TJ, C::MINB><<<grid, C::T, 0, stream>>>(a);
+    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<false>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
   count_launch();
-  return cudaGetLastError();
+  if (e != cudaSuccess) return e;
+
+  // Any i-block split between CTAs needs the fixup pass.
+  bool split = false;
+  for (int64_t b = 0; b < g.n_iblocks && !split; ++b)
+    split = host_cta_of(b * g.n_tiles, grid, g.units) != host_cta_of(b * g.n_tiles + g.n_tiles - 1, grid, g.units);
+  if (split) {
+    cfg.gridDim = dim3((unsigned)((a.n_i + 255) / 256));
+    cfg.blockDim = dim3(256);
+    e = cudaLaunchKernelEx(&cfg, fixup_kernel<R, IB>, a);
+    count_launch();
+  }
+  return e;
 }
 
 template <typename R>
 int64_t step_workspace_bytes(int64_t n_i) {
   const StepGeometry g = step_geometry<R>(n_i, 1);
-  const int64_t counters = ((g.n_iblocks * 4 + 255) / 256) * 256;
+  const int64_t counters = counters_bytes(g.n_iblocks);
   const int64_t slots = 2 * (int64_t)max_grid<R>() * 3 * g.i_block * 8;
   return counters + slots;
 }

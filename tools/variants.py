@@ -1,0 +1,140 @@
+"""Build and time kernel tuning variants (-D overrides of nbody_force.cu knobs).
+
+  python tools/variants.py build            # here: compile every variant .so
+  python tools/variants.py run [CONFIG...]  # on the GPU: time each variant
+
+Each variant is a full copy of libnbody_b200.so under tools/variants/."""
+import ctypes, json, os, subprocess, sys
+from concurrent.futures import ThreadPoolExecutor
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+sys.path.insert(0, REPO)
+OUT = os.path.join(HERE, "variants")
+
+VARIANTS = {
+    "base": {},
+    "ch64": {"NB_CHUNK": 64},
+    "ch128": {"NB_CHUNK": 128},
+    "k8": {"NB_F32_K": 8},
+    "k6_minb4": {"NB_F32_MINB": 4},
+    "k4_minb5": {"NB_F32_K": 4, "NB_F32_MINB": 5},
+    "k6_tj128": {"NB_F32_TJ": 128},
+    "k6_u8": {"NB_F32_UNROLL": 8},
+    "k6_pipe": {"NB_F32_PIPE": 1},
+    "f64_k2_minb4": {"NB_F64_K": 2, "NB_F64_MINB": 4},
+    "f64_k6": {"NB_F64_K": 6, "NB_F64_MINB": 2},
+    "f64_u2": {"NB_F64_UNROLL": 2},
+}
+
+
+def build_one(name, defs):
+    from paper_2203_08263_b200 import _build as B
+    objdir = os.path.join(OUT, name)
+    os.makedirs(objdir, exist_ok=True)
+    dflags = [f"-D{k}={v}" for k, v in defs.items()]
+    objs = []
+    for src in B.SOURCES:
+        o = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [B.NVCC, *B.ARCH, *B.FLAGS, *dflags, "-Xptxas", "-v", "-c", os.path.join(B.CSRC, src), "-o", o]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            return name, "FAILED " + r.stderr[-2000:]
+        if src == "nbody_force.cu":
+            log = r.stderr
+        objs.append(o)
+    lib = os.path.join(OUT, f"lib_{name}.so")
+    r = subprocess.run([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-o", lib, *objs], capture_output=True, text=True)
+    if r.returncode:
+        return name, "LINK FAILED " + r.stderr
+    regs = []
+    lines = log.splitlines()
+    for i, ln in enumerate(lines):
+        if "Function properties for" in ln and "step_kernel" in ln:
+            tag = "f32" if "CoreF32" in ln else "f64"
+            mask = "M" if "ILb1E" in ln else "-"
+            spill = lines[i + 1].strip()
+            used = lines[i + 2].split("Used")[1].split(",")[0].strip() if i + 2 < len(lines) and "Used" in lines[i + 2] else "?"
+            regs.append(f"{tag}{mask}:{used}|{spill.split(',')[1].strip()}")
+    return name, " ".join(regs)
+
+
+def build():
+    with ThreadPoolExecutor(8) as ex:
+        for name, info in ex.map(lambda kv: build_one(*kv), VARIANTS.items()):
+            print(f"{name:16s} {info}")
+
+
+def run(configs):
+    import numpy as np
+    import torch
+    import paper_2203_08263_b200 as nb
+    from paper_2203_08263_b200.device import DeviceState, needs_self_mask
+    from paper_2203_08263_b200 import _native
+    results = {}
+    for cfgname in configs:
+        cfg = nb.BASELINE_CONFIGS[cfgname]
+        s = cfg.system()
+        dt = cfg.precision.dtype
+        sfx = "_f32" if dt == np.float32 else "_f64"
+        if sfx == "_f64" and cfgname != "C3-f64":
+            pass
+        ref_state = DeviceState(s.position_matrix().astype(dt), np.stack(s.velocities, 1), s.masses, dt)
+        mask = needs_self_mask(s.masses, cfg.softening_sq, dt)
+        ref_acc = ref_state.accelerations(1.0, cfg.softening_sq, mask).cpu().numpy().astype(np.float64)
+        for name in VARIANTS:
+            path = os.path.join(OUT, f"lib_{name}.so")
+            if not os.path.exists(path):
+                continue
+            if sfx == "_f32" and name.startswith("f64"):
+                continue
+            if sfx == "_f64" and not (name.startswith("f64") or name == "base"):
+                continue
+            L = ctypes.CDLL(path)
+            fn = getattr(L, "nb_dev_simulate" + sfx)
+            fn.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                                   ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                                                   ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]
+            wsb = L.nb_dev_workspace_bytes
+            wsb.restype = ctypes.c_int64
+            wsb.argtypes = [ctypes.c_int, ctypes.c_int64]
+            nbytes = wsb(dt.itemsize, cfg.n)
+            st = DeviceState(s.position_matrix().astype(dt), np.stack(s.velocities, 1), s.masses, dt)
+            ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+            flag = ctypes.c_int(0)
+            step = getattr(L, "nb_dev_step" + sfx)
+            step.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                             ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                             ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+            acc = torch.zeros((cfg.n, 4), dtype=st.acc.dtype, device="cuda")
+            rc = step(st.pos_a.data_ptr(), cfg.n, 0, cfg.n, 0, cfg.n, 1.0, cfg.softening_sq, 0.0, 0, int(mask),
+                      None, 0, acc.data_ptr(), None, None, ws.data_ptr(), nbytes, 0)
+            torch.cuda.synchronize()
+            a = acc[:, :3].cpu().numpy().astype(np.float64)
+            dev = float(np.max(np.abs(a - ref_acc[:, :3]) / np.maximum(np.linalg.norm(ref_acc[:, :3], axis=1), 1e-300)[:, None]))
+
+            def sim():
+                r = fn(st.pos_a.data_ptr(), st.pos_b.data_ptr(), st.vel.data_ptr(), st.acc.data_ptr(), cfg.n, 1.0,
+                       cfg.dt, cfg.softening_sq, cfg.steps, int(mask), ws.data_ptr(), nbytes, 0, ctypes.byref(flag))
+                assert r == 0, r
+            sim(); sim()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ts = []
+            for _ in range(3):
+                e0.record(); sim(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1) / 1e3)
+            t = min(ts)
+            rate = cfg.interactions / t
+            peak = 148 * (128 if dt == np.float32 else 64) * 2 * 1.965e9
+            results[f"{cfgname}/{name}"] = {"rate": rate, "frac": 20 * rate / peak, "rc": rc, "dev_vs_base": dev}
+            print(f"{cfgname:8s} {name:16s} rate={rate:.4e} frac={20 * rate / peak:.4f} dev={dev:.2e}", flush=True)
+    with open(os.path.join(REPO, "gpurun_out", "variants.json"), "w") as f:
+        json.dump(results, f, indent=1)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    else:
+        run(sys.argv[2:] or ["C3-f32", "C2", "C3-f64"])
