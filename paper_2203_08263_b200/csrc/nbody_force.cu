@@ -45,7 +45,7 @@
 #define NB_F32_MINB 3
 #endif
 #ifndef NB_F32_UNROLL
-#define NB_F32_UNROLL 4
+#define NB_F32_UNROLL 8
 #endif
 #ifndef NB_F32_PIPE
 #define NB_F32_PIPE 0
