@@ -174,7 +174,7 @@ def run_ours(args) -> dict:
     import paper_2203_08263_b200 as nb
     from paper_2203_08263_b200 import _native
     from paper_2203_08263_b200._native import NB_STEP_FINAL_KICK, NB_STEP_FIRST, NB_STEP_KICK_DRIFT
-    from paper_2203_08263_b200.device import DeviceState, needs_self_mask
+    from paper_2203_08263_b200.device import DeviceState, kernel_flags, needs_self_mask
     from paper_2203_08263_b200.sharded import pad_system, run_sharded, shard_range
 
     world, rank, local = _dist_env()
@@ -195,7 +195,8 @@ def run_ours(args) -> dict:
     pos, vel, m = pad_system(pos0, vel0, m0, world)
     npad = pos.shape[0]
     i0, ni = shard_range(npad, rank, world)
-    mask = needs_self_mask(m0, cfg.softening_sq, dtype)
+    mask = kernel_flags(m, cfg.softening_sq, dtype) & ~1
+    mask |= 1 if needs_self_mask(m0, cfg.softening_sq, dtype) else 0
     state = DeviceState(pos, vel, m, dtype, device=dev, i_begin=i0, n_i=ni)
     pristine_pos = state.pos_a.clone()
     pristine_vel = state.vel.clone()

@@ -56,6 +56,14 @@ extern "C" {
 #define NB_STEP_KICK_DRIFT 2 /* step>0: v+=(a-acc4)*f, f=real(0.5*dt); then FIRST    */
 #define NB_STEP_FINAL_KICK 3 /* after the loop: v+=(a-acc4)*f; acc4<-a; p unchanged */
 
+/* Kernel flags (the `flags` argument of nb_dev_step_* / nb_dev_simulate_*). */
+#define NB_FLAG_EXCLUDE_SELF 1 /* skip j == i explicitly: required when (real)eps2 == 0 (the
+                                  self pair is 0*inf) or m*eps2^-1.5 overflows; otherwise the
+                                  self pair is included and adds exactly 0                   */
+#define NB_FLAG_UNIFORM_MASS 2 /* caller guarantees every m_j equals pos4[0].w: terms omit
+                                  m_j and the sum is scaled by m once (one FMUL2 less per
+                                  interaction pair)                                          */
+
 /* ---------------------------------------------------------------- host (FFI mirror) */
 
 /* Replaces _accel_cy.accel_soa (_accel_cy.pyx:114-152), called from
@@ -113,9 +121,7 @@ int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i);
  *   a_i = G * sum_j m_j (p_j - p_i) / (|p_j - p_i|^2 + eps2)^(3/2)
  *
  * mode         NB_MODE_ACCEL or one of NB_STEP_* (see above).
- * exclude_self 1: skip j == i explicitly (required when eps2 == 0, where the
- *              self pair is 0*inf); 0: self pair included, which adds exactly 0
- *              when (real)eps2 > 0 and max_m * eps2^-1.5 is finite.
+ * flags        NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS (see above).
  * carry        optional FP64 3*n_i buffer (SoA: x then y then z) of partial sums
  *              (without G):
  *              carry_mode 0: unused; 1: write the partial sums here and do not
@@ -129,12 +135,12 @@ int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i);
  * stream       a cudaStream_t (NULL = legacy default stream). */
 int nb_dev_step_f32(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i,
                     int64_t j_begin, int64_t j_count, double g, double eps2, double dt,
-                    int mode, int exclude_self, double* carry, int carry_mode, void* acc4,
+                    int mode, int flags, double* carry, int carry_mode, void* acc4,
                     void* vel4, void* pos4_next, void* workspace, int64_t workspace_bytes,
                     void* stream);
 int nb_dev_step_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i,
                     int64_t j_begin, int64_t j_count, double g, double eps2, double dt,
-                    int mode, int exclude_self, double* carry, int carry_mode, void* acc4,
+                    int mode, int flags, double* carry, int carry_mode, void* acc4,
                     void* vel4, void* pos4_next, void* workspace, int64_t workspace_bytes,
                     void* stream);
 
@@ -143,11 +149,11 @@ int nb_dev_step_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_
  * return (stream-ordered) the final positions are in pos4_a if steps is even,
  * else in pos4_b; *final_in_b reports which (may be NULL). */
 int nb_dev_simulate_f32(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n,
-                        double g, double dt, double eps2, int64_t steps, int exclude_self,
+                        double g, double dt, double eps2, int64_t steps, int flags,
                         void* workspace, int64_t workspace_bytes, void* stream,
                         int* final_in_b);
 int nb_dev_simulate_f64(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n,
-                        double g, double dt, double eps2, int64_t steps, int exclude_self,
+                        double g, double dt, double eps2, int64_t steps, int flags,
                         void* workspace, int64_t workspace_bytes, void* stream,
                         int* final_in_b);
 

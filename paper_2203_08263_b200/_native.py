@@ -20,6 +20,8 @@ NB_MODE_ACCEL = 0
 NB_STEP_FIRST = 1
 NB_STEP_KICK_DRIFT = 2
 NB_STEP_FINAL_KICK = 3
+NB_FLAG_EXCLUDE_SELF = 1
+NB_FLAG_UNIFORM_MASS = 2
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64

@@ -55,7 +55,7 @@ cudaError_t bind_device_of(const void* p) {
 
 template <typename R>
 int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
-             int64_t j_count, double g, double eps2, double dt, int mode, int exclude_self,
+             int64_t j_count, double g, double eps2, double dt, int mode, int flags,
              double* carry, int carry_mode, void* acc4, void* vel4, void* pos4_next,
              void* workspace, int64_t workspace_bytes, void* stream) {
   if (n_all < 1 || i_begin < 0 || n_i < 0 || i_begin + n_i > n_all)
@@ -93,16 +93,16 @@ int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int6
   a.acc = static_cast<V4<R>*>(acc4);
   a.vel = static_cast<V4<R>*>(vel4);
   a.pos_next = static_cast<V4<R>*>(pos4_next);
-  a.counters = static_cast<unsigned*>(workspace);
   a.slots = reinterpret_cast<double*>(static_cast<char*>(workspace) + counters_bytes(geo.n_iblocks));
-  cudaError_t e = launch_step<R>(a, exclude_self != 0, static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_step<R>(a, flags & (NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS),
+                                 static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "launch_step");
   return NB_OK;
 }
 
 template <typename R>
 int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, double g, double dt,
-                 double eps2, int64_t steps, int exclude_self, void* ws, int64_t ws_bytes, void* stream,
+                 double eps2, int64_t steps, int flags, void* ws, int64_t ws_bytes, void* stream,
                  int* final_in_b) {
   if (steps < 1) return fail(NB_ERR_ARG, "steps must be >= 1");
   if (!(dt > 0.0)) return fail(NB_ERR_ARG, "dt must be positive");
@@ -110,29 +110,34 @@ int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, do
   void* nxt = pos_b;
   for (int64_t s = 0; s < steps; ++s) {
     const int mode = s == 0 ? NB_STEP_FIRST : NB_STEP_KICK_DRIFT;
-    int rc = dev_step<R>(cur, n, 0, n, 0, n, g, eps2, dt, mode, exclude_self, nullptr, 0, acc4, vel4, nxt, ws,
+    int rc = dev_step<R>(cur, n, 0, n, 0, n, g, eps2, dt, mode, flags, nullptr, 0, acc4, vel4, nxt, ws,
                          ws_bytes, stream);
     if (rc) return rc;
     void* t = cur; cur = nxt; nxt = t;
   }
-  int rc = dev_step<R>(cur, n, 0, n, 0, n, g, eps2, dt, NB_STEP_FINAL_KICK, exclude_self, nullptr, 0, acc4,
+  int rc = dev_step<R>(cur, n, 0, n, 0, n, g, eps2, dt, NB_STEP_FINAL_KICK, flags, nullptr, 0, acc4,
                        vel4, nullptr, ws, ws_bytes, stream);
   if (rc) return rc;
   if (final_in_b) *final_in_b = cur == pos_b ? 1 : 0;
   return NB_OK;
 }
 
-// Whether the self pair can be included without a mask: (R)eps2 > 0 and the
-// largest self term m*eps2^-1.5 is finite with margin (else 0*inf = NaN).
+// Kernel flags for a host system: NB_FLAG_EXCLUDE_SELF unless the self pair
+// adds exactly 0 ((R)eps2 > 0 and the largest self term m*eps2^-1.5 is finite
+// with margin, else 0*inf = NaN), and NB_FLAG_UNIFORM_MASS when all masses are
+// equal (m is then applied once per body instead of once per pair).
 template <typename R>
-bool needs_mask(const R* m, int64_t n, double eps2) {
+int host_flags(const R* m, int64_t n, double eps2) {
   const double e = (double)(R)eps2;
-  if (!(e > 0.0)) return true;
   double mmax = 0.0;
-  for (int64_t i = 0; i < n; ++i) mmax = m[i] > mmax ? (double)m[i] : mmax;
+  bool uniform = true;
+  for (int64_t i = 0; i < n; ++i) {
+    mmax = m[i] > mmax ? (double)m[i] : mmax;
+    uniform = uniform && m[i] == m[0];
+  }
   const double big = sizeof(R) == 4 ? 1e30 : 1e300;
-  const double term = mmax * (1.0 / e) / std::sqrt(e);  // FP64 evaluation of the bound
-  return !(term < big);
+  const bool mask = !(e > 0.0) || !(mmax * (1.0 / e) / std::sqrt(e) < big);
+  return (mask ? NB_FLAG_EXCLUDE_SELF : 0) | (uniform ? NB_FLAG_UNIFORM_MASS : 0);
 }
 
 // RAII bag of device allocations for the host-pointer entry points.
@@ -186,7 +191,7 @@ int host_accel(const R* px, const R* py, const R* pz, const R* pos_aos, const R*
     NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, static_cast<R*>(dm), static_cast<V4<R>*>(dpos), n, 0));
   }
   NB_CUDA(cudaMemset(ws, 0, wsb));
-  if ((rc = dev_step<R>(dpos, n, 0, n, 0, n, g, eps2, 0.0, NB_MODE_ACCEL, needs_mask<R>(m, n, eps2) ? 1 : 0,
+  if ((rc = dev_step<R>(dpos, n, 0, n, 0, n, g, eps2, 0.0, NB_MODE_ACCEL, host_flags<R>(m, n, eps2),
                         nullptr, 0, dacc, nullptr, nullptr, ws, wsb, nullptr)))
     return rc;
   NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(dacc), d0, d0 + n, d0 + 2 * n, n, 0));
@@ -273,7 +278,7 @@ int host_simulate(R* px, R* py, R* pz, R* vx, R* vy, R* vz, const R* m, int64_t 
   NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, nullptr, static_cast<V4<R>*>(dv), n, 0));
   NB_CUDA(cudaMemset(ws, 0, wsb));
   int in_b = 0;
-  if ((rc = dev_simulate<R>(pa, pb, dv, da, n, g, dt, eps2, steps, needs_mask<R>(m, n, eps2) ? 1 : 0, ws, wsb,
+  if ((rc = dev_simulate<R>(pa, pb, dv, da, n, g, dt, eps2, steps, host_flags<R>(m, n, eps2), ws, wsb,
                             nullptr, &in_b)))
     return rc;
   NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(in_b ? pb : pa), d0, d0 + n, d0 + 2 * n, n, 0));
@@ -381,29 +386,29 @@ int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i) {
 }
 
 int nb_dev_step_f32(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin, int64_t j_count,
-                    double g, double eps2, double dt, int mode, int exclude_self, double* carry, int carry_mode,
+                    double g, double eps2, double dt, int mode, int flags, double* carry, int carry_mode,
                     void* acc4, void* vel4, void* pos4_next, void* workspace, int64_t workspace_bytes,
                     void* stream) {
-  return dev_step<float>(pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, exclude_self, carry,
+  return dev_step<float>(pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, flags, carry,
                          carry_mode, acc4, vel4, pos4_next, workspace, workspace_bytes, stream);
 }
 int nb_dev_step_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin, int64_t j_count,
-                    double g, double eps2, double dt, int mode, int exclude_self, double* carry, int carry_mode,
+                    double g, double eps2, double dt, int mode, int flags, double* carry, int carry_mode,
                     void* acc4, void* vel4, void* pos4_next, void* workspace, int64_t workspace_bytes,
                     void* stream) {
-  return dev_step<double>(pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, exclude_self, carry,
+  return dev_step<double>(pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, flags, carry,
                           carry_mode, acc4, vel4, pos4_next, workspace, workspace_bytes, stream);
 }
 int nb_dev_simulate_f32(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n, double g, double dt,
-                        double eps2, int64_t steps, int exclude_self, void* workspace, int64_t workspace_bytes,
+                        double eps2, int64_t steps, int flags, void* workspace, int64_t workspace_bytes,
                         void* stream, int* final_in_b) {
-  return dev_simulate<float>(pos4_a, pos4_b, vel4, acc4, n, g, dt, eps2, steps, exclude_self, workspace,
+  return dev_simulate<float>(pos4_a, pos4_b, vel4, acc4, n, g, dt, eps2, steps, flags, workspace,
                              workspace_bytes, stream, final_in_b);
 }
 int nb_dev_simulate_f64(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n, double g, double dt,
-                        double eps2, int64_t steps, int exclude_self, void* workspace, int64_t workspace_bytes,
+                        double eps2, int64_t steps, int flags, void* workspace, int64_t workspace_bytes,
                         void* stream, int* final_in_b) {
-  return dev_simulate<double>(pos4_a, pos4_b, vel4, acc4, n, g, dt, eps2, steps, exclude_self, workspace,
+  return dev_simulate<double>(pos4_a, pos4_b, vel4, acc4, n, g, dt, eps2, steps, flags, workspace,
                               workspace_bytes, stream, final_in_b);
 }
 int nb_dev_drift_f32(void* pos4, void* vel4, const void* acc4, int64_t n, double dt, void* stream) {

@@ -116,7 +116,7 @@ __device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
 // K target bodies per thread as K/2 packed pairs.  The FP64 segment sums live in
 // shared memory (3*K doubles per thread, touched once per tile) so the inner
 // loop keeps its registers for the pairs and their temporaries.
-template <int K_, bool MASK, int UNROLL_>
+template <int K_, bool MASK, int UNROLL_, bool UNI>
 struct CoreF32 {
   using R = float;
   static constexpr int K = K_;
@@ -166,8 +166,9 @@ struct CoreF32 {
       upk(d2, d2a, d2b);
       const f2x r = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
       const f2x r2 = mul2(r, r);
-      const f2x mr = mul2(r, mj);
-      f2x w = mul2(mr, r2);
+      // UNI (all masses equal): m is applied once to the finished sum, saving
+      // one FMUL2 of 12 per interaction pair.
+      f2x w = UNI ? mul2(r2, r) : mul2(mul2(r, mj), r2);
       if (MASK) {
         float wa, wb;
         upk(w, wa, wb);
@@ -203,8 +204,7 @@ struct CoreF32 {
 #pragma unroll
     for (int q = 0; q < KP; ++q) {
       const f2x r2 = mul2(r[q], r[q]);
-      const f2x mr = mul2(r[q], mj);
-      f2x w = mul2(mr, r2);
+      f2x w = UNI ? mul2(r2, r[q]) : mul2(mul2(r[q], mj), r2);
       if (MASK) {
         float wa, wb;
         upk(w, wa, wb);
@@ -261,7 +261,7 @@ struct CoreF32 {
 };
 
 // ---------------------------------------------------------------- FP64 core
-template <int K_, bool MASK, int UNROLL_>
+template <int K_, bool MASK, int UNROLL_, bool UNI>
 struct CoreF64 {
   using R = double;
   static constexpr int K = K_;
@@ -303,7 +303,7 @@ struct CoreF64 {
       const double y = rsqrt_seed(d2);
       const double t = y * y;
       const double e = fma(-d2, t, 1.0);
-      const double my3 = pj.w * (t * y);
+      const double my3 = UNI ? t * y : pj.w * (t * y);
       const double q = e * fma(e, 1.875, 1.5);
       double w = fma(my3, q, my3);
       if (MASK && jj == selfj[k]) w = 0.0;
@@ -329,7 +329,9 @@ __device__ __forceinline__ void finalize_body(const StepArgs<R>& a, int64_t il, 
     a.carry[2 * a.n_i + il] = tz;
     return;
   }
-  const R ax = (R)(tx * a.g), ay = (R)(ty * a.g), az = (R)(tz * a.g);
+  // Uniform-mass kernels left m_j out of every term: apply it once here.
+  const double gm = a.uniform_mass ? a.g * (double)a.pos[0].w : a.g;
+  const R ax = (R)(tx * gm), ay = (R)(ty * gm), az = (R)(tz * gm);
   V4<R> an;
   an.x = ax; an.y = ay; an.z = az; an.w = R(0);
   if (a.mode != NB_STEP_MODE_ACCEL) {
@@ -513,27 +515,27 @@ __global__ void __launch_bounds__(256) fixup_kernel(const StepArgs<R> a) {
 // ---------------------------------------------------------------- configurations
 // FP32: 128 threads x 8 bodies (4 FFMA2 pairs) = 1024-body i-blocks, 256-body tiles.
 // FP64: 128 threads x 4 bodies = 512-body i-blocks, 128-body tiles.
-template <bool M> struct CoreF32M : CoreF32<NB_F32_K, M, NB_F32_UNROLL> {
+template <bool M, bool U> struct CoreF32M : CoreF32<NB_F32_K, M, NB_F32_UNROLL, U> {
   static constexpr bool MASK_SELF = M;
 };
-template <bool M> struct CoreF64M : CoreF64<NB_F64_K, M, NB_F64_UNROLL> {
+template <bool M, bool U> struct CoreF64M : CoreF64<NB_F64_K, M, NB_F64_UNROLL, U> {
   static constexpr bool MASK_SELF = M;
 };
 
 template <typename R> struct Cfg;
 template <> struct Cfg<float> {
   static constexpr int T = NB_F32_T, TJ = NB_F32_TJ, MINB = NB_F32_MINB;
-  template <bool M> using Core = CoreF32M<M>;
+  template <bool M, bool U> using Core = CoreF32M<M, U>;
 };
 template <> struct Cfg<double> {
   static constexpr int T = NB_F64_T, TJ = NB_F64_TJ, MINB = NB_F64_MINB;
-  template <bool M> using Core = CoreF64M<M>;
+  template <bool M, bool U> using Core = CoreF64M<M, U>;
 };
 
-template <typename R, bool M>
+template <typename R, bool M, bool U>
 static const void* kernel_ptr() {
   using C = Cfg<R>;
-  return reinterpret_cast<const void*>(&step_kernel<typename C::template Core<M>, C::T, C::TJ, C::MINB, NB_CHUNK>);
+  return reinterpret_cast<const void*>(&step_kernel<typename C::template Core<M, U>, C::T, C::TJ, C::MINB, NB_CHUNK>);
 }
 
 template <typename R>
@@ -541,7 +543,7 @@ StepGeometry step_geometry(int64_t n_i, int64_t j_count) {
   using C = Cfg<R>;
   StepGeometry g{};
   g.threads = C::T;
-  g.i_block = C::T * C::template Core<false>::K;
+  g.i_block = C::T * C::template Core<false, false>::K;
   g.tile = C::TJ;
   g.n_iblocks = (n_i + g.i_block - 1) / g.i_block;
   g.n_tiles = j_count > 0 ? (j_count + NB_CHUNK - 1) / NB_CHUNK : 1;  // stream-K chunks
@@ -558,10 +560,11 @@ int max_grid() {
   if (cached[dev]) return cached[dev];
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int best = 1;
-  for (int m = 0; m < 2; ++m) {
+  const void* fns[4] = {kernel_ptr<R, false, false>(), kernel_ptr<R, true, false>(),
+                        kernel_ptr<R, false, true>(), kernel_ptr<R, true, true>()};
+  for (int m = 0; m < 4; ++m) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m ? kernel_ptr<R, true>() : kernel_ptr<R, false>(),
-                                                  Cfg<R>::T, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[m], Cfg<R>::T, 0);
     if (per_sm < 1) per_sm = 1;
     best = best > sms * per_sm ? best : sms * per_sm;
   }
@@ -580,7 +583,7 @@ static inline int64_t host_cta_of(int64_t u, int64_t grid, int64_t units) {
 }
 
 template <typename R>
-cudaError_t launch_step(StepArgs<R> a, bool mask_self, cudaStream_t stream) {
+cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   const StepGeometry g = step_geometry<R>(a.n_i, a.j_count);
   a.n_tiles = g.n_tiles;
   a.n_iblocks = g.n_iblocks;
@@ -589,7 +592,9 @@ cudaError_t launch_step(StepArgs<R> a, bool mask_self, cudaStream_t stream) {
   if ((int64_t)grid > g.units) grid = (int)g.units;
   a.grid = grid;
   using C = Cfg<R>;
-  constexpr int IB = C::T * C::template Core<false>::K;
+  constexpr int IB = C::T * C::template Core<false, false>::K;
+  const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
+  a.uniform_mass = uni ? 1 : 0;
 
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -602,10 +607,14 @@ cudaError_t launch_step(StepArgs<R> a, bool mask_self, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e;
-  if (mask_self)
-    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<true>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
+  if (mask_self && uni)
+    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<true, true>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
+  else if (mask_self)
+    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<true, false>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
+  else if (uni)
+    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<false, true>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
   else
-    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<false>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
+    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<false, false>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
   count_launch();
   if (e != cudaSuccess) return e;
 
@@ -632,8 +641,8 @@ int64_t step_workspace_bytes(int64_t n_i) {
 
 template StepGeometry step_geometry<float>(int64_t, int64_t);
 template StepGeometry step_geometry<double>(int64_t, int64_t);
-template cudaError_t launch_step<float>(StepArgs<float>, bool, cudaStream_t);
-template cudaError_t launch_step<double>(StepArgs<double>, bool, cudaStream_t);
+template cudaError_t launch_step<float>(StepArgs<float>, int, cudaStream_t);
+template cudaError_t launch_step<double>(StepArgs<double>, int, cudaStream_t);
 template int64_t step_workspace_bytes<float>(int64_t);
 template int64_t step_workspace_bytes<double>(int64_t);
 

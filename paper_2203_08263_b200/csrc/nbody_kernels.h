@@ -23,12 +23,12 @@ struct StepArgs {
   double g;          // applied to the FP64 sum, then rounded to R
   R dt, half, f;     // (R)dt, (R)0.5, (R)(0.5*dt)  (_accel_cy.pyx:211-212; __init__.py:223)
   int mode, carry_mode;
+  int uniform_mass;  // 1: every m_j equals pos[0].w; terms omit m_j, the sum is scaled once
   double* carry;     // 3*n_i FP64 partial sums (SoA), carry_mode 1/2
   V4<R>* acc;        // n_i: a_prev in, a out
   V4<R>* vel;        // n_i
   V4<R>* pos_next;   // n_all: rows of this shard written by drift modes
   double* slots;     // stream-K partial slots (workspace)
-  unsigned* counters;  // per i-block arrival counters (workspace, zero between launches)
   int64_t units, n_tiles, n_iblocks;
   int64_t grid;
 };
@@ -39,9 +39,10 @@ struct StepGeometry {
 };
 
 template <typename R> StepGeometry step_geometry(int64_t n_i, int64_t j_count);
-template <typename R> cudaError_t launch_step(StepArgs<R> a, bool mask_self, cudaStream_t s);
+// flags: bit 0 exclude the self pair explicitly, bit 1 uniform masses.
+template <typename R> cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t s);
 template <typename R> int64_t step_workspace_bytes(int64_t n_i);
-// Byte offset of the slot area inside the workspace (counters come first).
+// Byte offset of the slot area inside the workspace (a 256-byte-aligned header).
 inline int64_t counters_bytes(int64_t n_iblocks) { return ((n_iblocks * 4 + 255) / 256) * 256; }
 
 // Stand-alone O(N) kernels (nbody_update.cu).

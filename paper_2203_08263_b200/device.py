@@ -25,9 +25,10 @@ import numpy as np
 import torch
 
 from . import _native
-from ._native import NB_MODE_ACCEL, NB_STEP_FINAL_KICK, NB_STEP_FIRST, NB_STEP_KICK_DRIFT
+from ._native import (NB_FLAG_EXCLUDE_SELF, NB_FLAG_UNIFORM_MASS, NB_MODE_ACCEL, NB_STEP_FINAL_KICK,
+                      NB_STEP_FIRST, NB_STEP_KICK_DRIFT)
 
-__all__ = ["DeviceState", "needs_self_mask", "pack_bodies", "TORCH_DTYPE"]
+__all__ = ["DeviceState", "needs_self_mask", "kernel_flags", "pack_bodies", "TORCH_DTYPE"]
 
 TORCH_DTYPE = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
 
@@ -43,6 +44,17 @@ def needs_self_mask(masses: np.ndarray, eps2: float, dtype) -> bool:
     big = 1e30 if dtype == np.float32 else 1e300
     mmax = float(np.max(masses)) if masses.size else 0.0
     return not (mmax * (1.0 / e) / np.sqrt(e) < big)
+
+
+def kernel_flags(masses: np.ndarray, eps2: float, dtype, allow_uniform: bool = True) -> int:
+    """nb_dev_step flags for a system: NB_FLAG_EXCLUDE_SELF when the self pair
+    must be masked, NB_FLAG_UNIFORM_MASS when every mass is identical (m is then
+    applied once per body; C5's Plummer sphere has m = 1/N for all bodies)."""
+    m = np.asarray(masses)
+    flags = NB_FLAG_EXCLUDE_SELF if needs_self_mask(m, eps2, dtype) else 0
+    if allow_uniform and m.size and bool(np.all(m == m[0])):
+        flags |= NB_FLAG_UNIFORM_MASS
+    return flags
 
 
 def pack_bodies(pos: np.ndarray, w: Optional[np.ndarray], dtype, pin: bool) -> torch.Tensor:
@@ -110,7 +122,7 @@ class DeviceState:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     # -------------------------------------------------------------- kernels
-    def step(self, g: float, eps2: float, dt: float, mode: int, exclude_self: bool,
+    def step(self, g: float, eps2: float, dt: float, mode: int, flags: int,
              j_begin: Optional[int] = None, j_count: Optional[int] = None, carry_mode: int = 0,
              acc_out: Optional[torch.Tensor] = None) -> None:
         """One fused force(+update) launch on the current positions (nb_dev_step)."""
@@ -119,28 +131,28 @@ class DeviceState:
         acc = self.acc if acc_out is None else acc_out
         drift = mode in (NB_STEP_FIRST, NB_STEP_KICK_DRIFT)
         _native.call("nb_dev_step" + self.sfx, self.pos_cur.data_ptr(), self.n, self.i_begin, self.n_i,
-                     j_begin % self.n, j_count, g, eps2, dt, mode, int(exclude_self),
+                     j_begin % self.n, j_count, g, eps2, dt, mode, int(flags),
                      self.carry.data_ptr() if carry_mode else None, carry_mode, acc.data_ptr(),
                      self.vel.data_ptr() if mode != NB_MODE_ACCEL else None,
                      self.pos_next.data_ptr() if drift else None,
                      self.ws.data_ptr(), self.ws_bytes, self.stream_ptr())
 
-    def simulate(self, g: float, dt: float, eps2: float, steps: int, exclude_self: bool) -> None:
+    def simulate(self, g: float, dt: float, eps2: float, steps: int, flags: int) -> None:
         """Whole single-device velocity-Verlet run (nb_dev_simulate): steps+1 launches."""
         if self.i_begin != 0 or self.n_i != self.n:
             raise ValueError("DeviceState.simulate runs an unsharded system; use sharded.simulate")
         final_in_b = ctypes.c_int(0)
         _native.call("nb_dev_simulate" + self.sfx, self.pos_cur.data_ptr(), self.pos_next.data_ptr(),
                      self.vel.data_ptr(), self.acc.data_ptr(), self.n, g, dt, eps2, steps,
-                     int(exclude_self), self.ws.data_ptr(), self.ws_bytes, self.stream_ptr(),
+                     int(flags), self.ws.data_ptr(), self.ws_bytes, self.stream_ptr(),
                      ctypes.byref(final_in_b))
         if steps % 2 == 1:
             self.swap()
 
-    def accelerations(self, g: float, eps2: float, exclude_self: bool) -> torch.Tensor:
+    def accelerations(self, g: float, eps2: float, flags: int) -> torch.Tensor:
         """(n_i, 4) device accelerations of the current positions (mode ACCEL)."""
         out = torch.empty((max(self.n_i, 1), 4), dtype=self.acc.dtype, device=self.device)
-        self.step(g, eps2, 0.0, NB_MODE_ACCEL, exclude_self, j_begin=0, j_count=self.n, acc_out=out)
+        self.step(g, eps2, 0.0, NB_MODE_ACCEL, flags, j_begin=0, j_count=self.n, acc_out=out)
         return out[: self.n_i]
 
     def energy(self, g: float, eps2: float) -> Tuple[float, float, Tuple[float, float, float]]:

@@ -183,7 +183,7 @@ def compute_accelerations(sys_, params, variant: Optional[KernelVariant] = None,
                           out: Optional[AccelerationBuffer] = None) -> AccelerationBuffer:
     """Softened all-pairs accelerations of the current state, written into
     ``out`` (allocated if None) in the system precision; returns ``out``."""
-    from .device import DeviceState, needs_self_mask
+    from .device import DeviceState, kernel_flags
     dtype = _dtype(sys_)
     if out is None:
         out = AccelerationBuffer.allocate(_count(sys_), _value(sys_.precision))
@@ -192,7 +192,7 @@ def compute_accelerations(sys_, params, variant: Optional[KernelVariant] = None,
     m = np.asarray(sys_.masses, dtype)
     eps2 = params.softening_sq
     st = DeviceState(pos, np.zeros_like(pos), m, dtype)
-    a = st.accelerations(params.gravitational_constant, eps2, needs_self_mask(m, eps2, dtype))
+    a = st.accelerations(params.gravitational_constant, eps2, kernel_flags(m, eps2, dtype))
     host = a[:, :3].cpu().numpy()
     out.x[...] = host[:, 0]
     out.y[...] = host[:, 1]
@@ -226,7 +226,7 @@ def simulate_arrays(positions, velocities, masses, softening_sq: float, dt: floa
     final (N,3) positions and velocities out, in the input precision (float32 or
     float64; ``precision`` overrides).  Runs sharded over the process group when
     torch.distributed is initialised with more than one rank."""
-    from .device import DeviceState, needs_self_mask
+    from .device import DeviceState, kernel_flags
     pos = np.asarray(positions)
     if precision is not None:
         dtype = Precision(_value(precision)).dtype
@@ -247,7 +247,7 @@ def simulate_arrays(positions, velocities, masses, softening_sq: float, dt: floa
         from .sharded import simulate_sharded
         return simulate_sharded(pos, vel, m, dtype, G, dt, softening_sq, steps, group=group)
     st = DeviceState(pos, vel, m, dtype)
-    st.simulate(G, dt, softening_sq, steps, needs_self_mask(m, softening_sq, dtype))
+    st.simulate(G, dt, softening_sq, steps, kernel_flags(m, softening_sq, dtype))
     return st.positions_host(), st.velocities_host()
 
 

@@ -55,7 +55,7 @@ def pad_system(pos: np.ndarray, vel: np.ndarray, m: np.ndarray, world: int):
             np.concatenate([m, np.zeros(extra, m.dtype)]))
 
 
-def run_sharded(state, g: float, dt: float, eps2: float, steps: int, exclude_self: bool,
+def run_sharded(state, g: float, dt: float, eps2: float, steps: int, flags: int,
                 allgather: Callable, world: int) -> None:
     """Velocity-Verlet loop of kernels.simulate (kernels/__init__.py:240-252) on
     one shard.  ``state`` holds all positions and this rank's rows; ``allgather``
@@ -64,19 +64,19 @@ def run_sharded(state, g: float, dt: float, eps2: float, steps: int, exclude_sel
     n, i0, ni = state.n, state.i_begin, state.n_i
     if world == 1:
         for s in range(steps):
-            state.step(g, eps2, dt, NB_STEP_FIRST if s == 0 else NB_STEP_KICK_DRIFT, exclude_self)
+            state.step(g, eps2, dt, NB_STEP_FIRST if s == 0 else NB_STEP_KICK_DRIFT, flags)
             state.swap()
-        state.step(g, eps2, dt, NB_STEP_FINAL_KICK, exclude_self)
+        state.step(g, eps2, dt, NB_STEP_FINAL_KICK, flags)
         return
     pending = None
     for s in range(steps + 1):
         mode = NB_STEP_FIRST if s == 0 else (NB_STEP_KICK_DRIFT if s < steps else NB_STEP_FINAL_KICK)
         # local sources first: rows [i0, i0+ni) of the current positions are ours
-        state.step(g, eps2, dt, mode, exclude_self, j_begin=i0, j_count=ni, carry_mode=1)
+        state.step(g, eps2, dt, mode, flags, j_begin=i0, j_count=ni, carry_mode=1)
         if pending is not None:
             pending.wait()
         # then every other source, as one circular range after the local slice
-        state.step(g, eps2, dt, mode, exclude_self, j_begin=(i0 + ni) % n, j_count=n - ni, carry_mode=2)
+        state.step(g, eps2, dt, mode, flags, j_begin=(i0 + ni) % n, j_count=n - ni, carry_mode=2)
         if mode != NB_STEP_FINAL_KICK:
             state.swap()
             pending = allgather(state.pos_cur, state.pos_cur[i0:i0 + ni])
@@ -94,14 +94,15 @@ def _torch_allgather(group):
 
 def simulate_sharded(positions: np.ndarray, velocities: np.ndarray, masses: np.ndarray, dtype,
                      g: float, dt: float, eps2: float, steps: int, group=None,
-                     exclude_self: Optional[bool] = None) -> Tuple[np.ndarray, np.ndarray]:
+                     flags: Optional[int] = None) -> Tuple[np.ndarray, np.ndarray]:
     """Multi-GPU simulate: every rank passes the full initial state and gets the
     full final (positions, velocities) back.  Uses the default process group
     (NCCL, one process per GPU) unless ``group`` is given."""
     import torch
     import torch.distributed as dist
 
-    from .device import DeviceState, needs_self_mask
+    from ._native import NB_FLAG_EXCLUDE_SELF
+    from .device import DeviceState, kernel_flags, needs_self_mask
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     n = positions.shape[0]
@@ -110,10 +111,12 @@ def simulate_sharded(positions: np.ndarray, velocities: np.ndarray, masses: np.n
                              np.asarray(masses, dtype), world)
     npad = pos.shape[0]
     i0, ni = shard_range(npad, rank, world)
-    if exclude_self is None:
-        exclude_self = needs_self_mask(m[:n], eps2, dtype)
+    if flags is None:
+        # uniform masses only if no massless padding was added
+        flags = kernel_flags(m, eps2, dtype) & ~NB_FLAG_EXCLUDE_SELF
+        flags |= NB_FLAG_EXCLUDE_SELF if needs_self_mask(m[:n], eps2, dtype) else 0
     state = DeviceState(pos, vel, m, dtype, i_begin=i0, n_i=ni)
-    run_sharded(state, g, dt, eps2, steps, exclude_self, _torch_allgather(group), world)
+    run_sharded(state, g, dt, eps2, steps, flags, _torch_allgather(group), world)
     vel_full = torch.empty((npad, 4), dtype=state.vel.dtype, device=state.device)
     dist.all_gather_into_tensor(vel_full, state.vel[:ni].contiguous(), group=group)
     out_pos = state.pos_cur[:n, :3].cpu().numpy()

@@ -402,6 +402,27 @@ def test_sharded_driver_on_one_gpu(prec, world):
     assert position_dev(got, ref.position_matrix()) <= tol
 
 
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_uniform_mass_path_matches_general_path(prec, oracle):
+    """NB_FLAG_UNIFORM_MASS (m applied once per body, used automatically for
+    equal-mass systems such as C5's Plummer sphere) agrees with the general
+    per-pair-mass kernel and with the oracle."""
+    from paper_2203_08263_b200.device import DeviceState
+    from paper_2203_08263_b200._native import NB_FLAG_UNIFORM_MASS
+    s = nb.plummer_sphere(20000, 3, nb.Precision(prec))
+    dtype = s.precision.dtype
+    st = DeviceState(s.position_matrix().astype(dtype), np.stack(s.velocities, 1), s.masses, dtype)
+    a_gen = st.accelerations(1.0, 1e-4, 0)[:, :3].cpu().numpy().astype(np.float64)
+    a_uni = st.accelerations(1.0, 1e-4, NB_FLAG_UNIFORM_MASS)[:, :3].cpu().numpy().astype(np.float64)
+    rows = np.arange(0, 20000, 97)
+    pos = s.position_matrix()
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)), s.masses, rows, 1.0, 1e-4)
+    tol = F64_ACC_TOL if prec == "double" else F32_ACC_TOL
+    assert nb_accel_dev(a_uni[rows], want) <= tol
+    assert nb_accel_dev(a_gen[rows], want) <= tol
+    assert nb_accel_dev(a_uni, a_gen) <= (1e-14 if prec == "double" else 2e-6)
+
+
 # --------------------------------------------------------------------------- plugin + diagnostics
 
 @pytest.mark.parametrize("prec", ["double", "single"])

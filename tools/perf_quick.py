@@ -3,7 +3,7 @@ import sys, os, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2203_08263_b200 as nb
-from paper_2203_08263_b200.device import DeviceState, needs_self_mask
+from paper_2203_08263_b200.device import DeviceState, kernel_flags
 
 PEAK32 = 148 * 128 * 2 * 1.965e9
 PEAK64 = PEAK32 / 2
@@ -13,7 +13,7 @@ for name in names:
     s = cfg.system()
     pos = s.position_matrix().astype(cfg.precision.dtype); vel = np.stack(s.velocities, 1)
     st = DeviceState(pos, vel, s.masses, cfg.precision.dtype)
-    mask = needs_self_mask(s.masses, cfg.softening_sq, cfg.precision.dtype)
+    mask = kernel_flags(s.masses, cfg.softening_sq, cfg.precision.dtype)
     p = cfg.params()
     for _ in range(2):
         st.simulate(1.0, p.dt, p.softening_sq, p.steps, mask)

@@ -69,7 +69,7 @@ def run(configs):
     import numpy as np
     import torch
     import paper_2203_08263_b200 as nb
-    from paper_2203_08263_b200.device import DeviceState, needs_self_mask
+    from paper_2203_08263_b200.device import DeviceState, kernel_flags
     from paper_2203_08263_b200 import _native
     results = {}
     for cfgname in configs:
@@ -80,7 +80,7 @@ def run(configs):
         if sfx == "_f64" and cfgname != "C3-f64":
             pass
         ref_state = DeviceState(s.position_matrix().astype(dt), np.stack(s.velocities, 1), s.masses, dt)
-        mask = needs_self_mask(s.masses, cfg.softening_sq, dt)
+        mask = kernel_flags(s.masses, cfg.softening_sq, dt)
         ref_acc = ref_state.accelerations(1.0, cfg.softening_sq, mask).cpu().numpy().astype(np.float64)
         for name in VARIANTS:
             path = os.path.join(OUT, f"lib_{name}.so")
