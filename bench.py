@@ -209,29 +209,25 @@ def run_ours(args) -> dict:
         state.acc.zero_()
         state.cur_is_a = True
 
-    launch_events = []
+    launch_ms_all = []
 
     def one_step(record_launches: bool):
-        """One simulate of the config on the resident state (steps+1 launches)."""
+        """One simulate of the config on the resident state (steps+1 launches).
+        N=1: the product's own C loop (nb_dev_simulate[_timed]); the timed
+        variant records a CUDA event between consecutive launches on the launch
+        stream and returns each launch's device time.  N>1: the sharded driver."""
         if world == 1:
-            evs = [torch.cuda.Event(enable_timing=True)] if record_launches else None
-            if evs:
-                evs[0].record()
-            for s in range(steps + 1):
-                mode = NB_STEP_FIRST if s == 0 else (NB_STEP_KICK_DRIFT if s < steps else NB_STEP_FINAL_KICK)
-                state.step(g, eps2, dt, mode, mask)
-                if mode != NB_STEP_FINAL_KICK:
-                    state.swap()
-                if evs is not None:
-                    e = torch.cuda.Event(enable_timing=True)
-                    e.record()
-                    evs.append(e)
-            if evs is not None:
-                launch_events.append(evs)
-        else:
-            def gather(full, local_rows):
-                return dist.all_gather_into_tensor(full, local_rows, async_op=True)
-            run_sharded(state, g, dt, eps2, steps, mask, gather, world)
+            if record_launches:
+                ms = state.simulate_timed(g, dt, eps2, steps, mask)
+                launch_ms_all.append(ms)
+                return sum(ms)
+            state.simulate(g, dt, eps2, steps, mask)
+            return None
+
+        def gather(full, local_rows):
+            return dist.all_gather_into_tensor(full, local_rows, async_op=True)
+        run_sharded(state, g, dt, eps2, steps, mask, gather, world)
+        return None
 
     def barrier():
         if world > 1:
@@ -251,17 +247,21 @@ def run_ours(args) -> dict:
     launches_before = _native.launch_count()
     barrier()
     torch.cuda.synchronize()
+    step_ms = []
     for k in range(args.steps):
         reset()
         flush.zero_()  # L2 flush between timed steps (outside the events)
         starts[k].record()
-        one_step(record_launches=(world == 1))
+        dev_ms = one_step(record_launches=(world == 1))
         ends[k].record()
+        step_ms.append(dev_ms)
     torch.cuda.synchronize()
     barrier()
     launches = _native.launch_count() - launches_before
     clk = clocks.stop()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    # N=1: events recorded back to back with the launches (first launch .. last
+    # launch); N>1: events bracketing the sharded loop on the compute stream.
+    step_ms = [m if m is not None else s.elapsed_time(e) for m, s, e in zip(step_ms, starts, ends)]
     total_s = sum(step_ms) / 1e3
     if world > 1:
         t = torch.tensor([total_s], dtype=torch.float64, device=dev)
@@ -271,9 +271,7 @@ def run_ours(args) -> dict:
     value = interactions / total_s
 
     # per-launch kernel durations (N=1): the dominant (only) kernel of the step
-    kernel_ms = []
-    for evs in launch_events:
-        kernel_ms += [a.elapsed_time(b) for a, b in zip(evs[:-1], evs[1:])]
+    kernel_ms = [x for ms in launch_ms_all for x in ms]
     peak = nominal_peak_tflops(pbytes)
     if kernel_ms:
         mean_launch_s = statistics.mean(kernel_ms) / 1e3
@@ -288,7 +286,7 @@ def run_ours(args) -> dict:
                        % (128 if pbytes == 4 else 64),
         "peak_measured_microbench": MEASURED_FFMA_TFLOPS if pbytes == 4 else MEASURED_DFMA_TFLOPS,
         "frac_of_measured_microbench": achieved / (MEASURED_FFMA_TFLOPS if pbytes == 4 else MEASURED_DFMA_TFLOPS),
-        "kernel": "nb::step_kernel (fused force + velocity-Verlet epilogue)",
+        "kernel": "nb::step_kernel (fused force + velocity-Verlet epilogue) + nb::fixup_kernel",
         "mean_launch_ms": mean_launch_s * 1e3,
         "algorithmic_flop_per_launch": FLOP_PER_INTERACTION * float(cfg.n) * cfg.n,
         "traffic": load_traffic(args.config),

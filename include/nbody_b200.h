@@ -157,6 +157,18 @@ int nb_dev_simulate_f64(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int6
                         void* workspace, int64_t workspace_bytes, void* stream,
                         int* final_in_b);
 
+/* nb_dev_simulate_* plus per-launch device timing: launch_ms (host, steps+1
+ * floats) receives the CUDA-event time of each force evaluation (fused step +
+ * fixup) measured on `stream`.  Synchronizes the stream before returning. */
+int nb_dev_simulate_timed_f32(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n,
+                              double g, double dt, double eps2, int64_t steps, int flags,
+                              void* workspace, int64_t workspace_bytes, void* stream,
+                              int* final_in_b, float* launch_ms);
+int nb_dev_simulate_timed_f64(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n,
+                              double g, double dt, double eps2, int64_t steps, int flags,
+                              void* workspace, int64_t workspace_bytes, void* stream,
+                              int* final_in_b, float* launch_ms);
+
 /* Stand-alone update kernels on packed arrays (n entries each): the kick-drift
  * of step_soa (_accel_cy.pyx:205-237) in place, and the trapezoidal kick of
  * _kick (kernels/__init__.py:220-227): v += (a_new - a_old) * real(factor). */

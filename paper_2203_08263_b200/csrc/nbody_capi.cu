@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "nbody_b200.h"
 #include "nbody_kernels.h"
@@ -100,26 +101,53 @@ int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int6
   return NB_OK;
 }
 
+// `events` (optional): steps+2 recorded events, one before every launch and one
+// after the last, so a caller can time each force evaluation on the stream.
 template <typename R>
 int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, double g, double dt,
                  double eps2, int64_t steps, int flags, void* ws, int64_t ws_bytes, void* stream,
-                 int* final_in_b) {
+                 int* final_in_b, cudaEvent_t* events = nullptr) {
   if (steps < 1) return fail(NB_ERR_ARG, "steps must be >= 1");
   if (!(dt > 0.0)) return fail(NB_ERR_ARG, "dt must be positive");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* cur = pos_a;
   void* nxt = pos_b;
   for (int64_t s = 0; s < steps; ++s) {
     const int mode = s == 0 ? NB_STEP_FIRST : NB_STEP_KICK_DRIFT;
+    if (events) NB_CUDA(cudaEventRecord(events[s], st));
     int rc = dev_step<R>(cur, n, 0, n, 0, n, g, eps2, dt, mode, flags, nullptr, 0, acc4, vel4, nxt, ws,
                          ws_bytes, stream);
     if (rc) return rc;
     void* t = cur; cur = nxt; nxt = t;
   }
+  if (events) NB_CUDA(cudaEventRecord(events[steps], st));
   int rc = dev_step<R>(cur, n, 0, n, 0, n, g, eps2, dt, NB_STEP_FINAL_KICK, flags, nullptr, 0, acc4,
                        vel4, nullptr, ws, ws_bytes, stream);
   if (rc) return rc;
+  if (events) NB_CUDA(cudaEventRecord(events[steps + 1], st));
   if (final_in_b) *final_in_b = cur == pos_b ? 1 : 0;
   return NB_OK;
+}
+
+template <typename R>
+int dev_simulate_timed(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, double g, double dt,
+                       double eps2, int64_t steps, int flags, void* ws, int64_t ws_bytes, void* stream,
+                       int* final_in_b, float* launch_ms) {
+  if (steps < 1) return fail(NB_ERR_ARG, "steps must be >= 1");
+  if (!launch_ms) return fail(NB_ERR_ARG, "launch_ms must hold steps+1 floats");
+  if (!pos_a) return fail(NB_ERR_ARG, "null device pointer");
+  if (cudaError_t be = bind_device_of(pos_a)) return cuda_fail(be, "pos4 is not a device pointer");
+  std::vector<cudaEvent_t> ev((size_t)steps + 2);
+  for (auto& e : ev) NB_CUDA(cudaEventCreate(&e));
+  int rc = dev_simulate<R>(pos_a, pos_b, vel4, acc4, n, g, dt, eps2, steps, flags, ws, ws_bytes, stream,
+                           final_in_b, ev.data());
+  if (!rc) {
+    cudaError_t e = cudaEventSynchronize(ev.back());
+    for (int64_t k = 0; k <= steps && e == cudaSuccess; ++k) e = cudaEventElapsedTime(&launch_ms[k], ev[k], ev[k + 1]);
+    if (e != cudaSuccess) rc = cuda_fail(e, "event timing");
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
 }
 
 // Kernel flags for a host system: NB_FLAG_EXCLUDE_SELF unless the self pair
@@ -410,6 +438,18 @@ int nb_dev_simulate_f64(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int6
                         void* stream, int* final_in_b) {
   return dev_simulate<double>(pos4_a, pos4_b, vel4, acc4, n, g, dt, eps2, steps, flags, workspace,
                               workspace_bytes, stream, final_in_b);
+}
+int nb_dev_simulate_timed_f32(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n, double g, double dt,
+                              double eps2, int64_t steps, int flags, void* workspace, int64_t workspace_bytes,
+                              void* stream, int* final_in_b, float* launch_ms) {
+  return dev_simulate_timed<float>(pos4_a, pos4_b, vel4, acc4, n, g, dt, eps2, steps, flags, workspace,
+                                   workspace_bytes, stream, final_in_b, launch_ms);
+}
+int nb_dev_simulate_timed_f64(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n, double g, double dt,
+                              double eps2, int64_t steps, int flags, void* workspace, int64_t workspace_bytes,
+                              void* stream, int* final_in_b, float* launch_ms) {
+  return dev_simulate_timed<double>(pos4_a, pos4_b, vel4, acc4, n, g, dt, eps2, steps, flags, workspace,
+                                    workspace_bytes, stream, final_in_b, launch_ms);
 }
 int nb_dev_drift_f32(void* pos4, void* vel4, const void* acc4, int64_t n, double dt, void* stream) {
   return dev_drift<float>(pos4, vel4, acc4, n, dt, stream);

@@ -149,6 +149,21 @@ class DeviceState:
         if steps % 2 == 1:
             self.swap()
 
+    def simulate_timed(self, g: float, dt: float, eps2: float, steps: int, flags: int) -> list:
+        """``simulate`` that also returns the CUDA-event time (ms) of each of the
+        steps+1 force evaluations, measured on this stream (synchronizes)."""
+        if self.i_begin != 0 or self.n_i != self.n:
+            raise ValueError("DeviceState.simulate_timed runs an unsharded system")
+        final_in_b = ctypes.c_int(0)
+        ms = (ctypes.c_float * (steps + 1))()
+        _native.call("nb_dev_simulate_timed" + self.sfx, self.pos_cur.data_ptr(), self.pos_next.data_ptr(),
+                     self.vel.data_ptr(), self.acc.data_ptr(), self.n, g, dt, eps2, steps,
+                     int(flags), self.ws.data_ptr(), self.ws_bytes, self.stream_ptr(),
+                     ctypes.byref(final_in_b), ms)
+        if steps % 2 == 1:
+            self.swap()
+        return list(ms)
+
     def accelerations(self, g: float, eps2: float, flags: int) -> torch.Tensor:
         """(n_i, 4) device accelerations of the current positions (mode ACCEL)."""
         out = torch.empty((max(self.n_i, 1), 4), dtype=self.acc.dtype, device=self.device)

@@ -276,6 +276,19 @@ def test_runs_are_bitwise_reproducible(prec):
     np.testing.assert_array_equal(a, b)
 
 
+def test_simulate_timed_matches_simulate():
+    from paper_2203_08263_b200.device import DeviceState, kernel_flags
+    s = cube(5000, 12, "single")
+    dt_ = s.precision.dtype
+    a = DeviceState(s.position_matrix().astype(dt_), np.stack(s.velocities, 1), s.masses, dt_)
+    b = DeviceState(s.position_matrix().astype(dt_), np.stack(s.velocities, 1), s.masses, dt_)
+    f = kernel_flags(s.masses, 1e-3, dt_)
+    a.simulate(1.0, 1e-3, 1e-3, 5, f)
+    ms = b.simulate_timed(1.0, 1e-3, 1e-3, 5, f)
+    assert len(ms) == 6 and all(t > 0 for t in ms)
+    np.testing.assert_array_equal(a.positions_host(), b.positions_host())
+
+
 def test_native_kernels_launched():
     before = _native.launch_count()
     nb.simulate(cube(64, 1, "single"), nb.SimParams(1.0, 1e-3, 1e-3, 2))

@@ -14,17 +14,12 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
+    "t64": {"NB_F32_T": 64, "NB_F32_MINB": 6},
+    "k4_t64": {"NB_F32_K": 4, "NB_F32_T": 64, "NB_F32_MINB": 8},
+    "k4": {"NB_F32_K": 4},
     "ch64": {"NB_CHUNK": 64},
-    "ch128": {"NB_CHUNK": 128},
-    "k8": {"NB_F32_K": 8},
+    "tj128_ch32": {"NB_F32_TJ": 128},
     "k6_minb4": {"NB_F32_MINB": 4},
-    "k4_minb5": {"NB_F32_K": 4, "NB_F32_MINB": 5},
-    "k6_tj128": {"NB_F32_TJ": 128},
-    "k6_u8": {"NB_F32_UNROLL": 8},
-    "k6_pipe": {"NB_F32_PIPE": 1},
-    "f64_k2_minb4": {"NB_F64_K": 2, "NB_F64_MINB": 4},
-    "f64_k6": {"NB_F64_K": 6, "NB_F64_MINB": 2},
-    "f64_u2": {"NB_F64_UNROLL": 2},
 }
 
 
