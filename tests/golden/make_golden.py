@@ -74,6 +74,8 @@ def main():
     consts["c1_checksum"] = nb.checksum(c1_final)
     c1_acc = acc_arrays(reference_accelerations(c1, c1p))
     consts["c1_oracle_acc0"] = [float(v) for v in c1_acc[0]]
+    from nbodybench.cli import CSV_HEADER
+    consts["csv_header"] = list(CSV_HEADER)
     with open(os.path.join(HERE, "reference_constants.json"), "w") as f:
         json.dump(consts, f, indent=1)
 
