@@ -190,6 +190,17 @@ int nb_dev_energy_f32(const void* pos4, const void* vel4, int64_t n, double g, d
 int nb_dev_energy_f64(const void* pos4, const void* vel4, int64_t n, double g, double eps2,
                       double* out6, void* workspace, int64_t workspace_bytes, void* stream);
 
+/* On-device initial conditions (BASELINE.json generators):
+ * splitmix64 in closed form (core.py:92-113), FP64, rounded once to the system
+ * precision.  NB_INIT_UNIFORM_CUBE: 7 draws per body, x = -1+2u, v = -0.1+0.2u,
+ * m = 0.5+u (bit-identical to paper_2203_08263_b200.core.uniform_cube);
+ * NB_INIT_PLUMMER: 3 draws per body, scale radius 1, v = 0, m = 1/n.
+ * Writes n packed bodies to pos4 (x,y,z,m) and vel4 (vx,vy,vz,0). */
+#define NB_INIT_UNIFORM_CUBE 0
+#define NB_INIT_PLUMMER 1
+int nb_dev_init_f32(int kind, uint64_t seed, int64_t n, void* pos4, void* vel4, void* stream);
+int nb_dev_init_f64(int kind, uint64_t seed, int64_t n, void* pos4, void* vel4, void* stream);
+
 /* ---------------------------------------------------------------- misc */
 
 const char* nb_last_error(void);

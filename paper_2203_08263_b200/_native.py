@@ -22,6 +22,8 @@ NB_STEP_KICK_DRIFT = 2
 NB_STEP_FINAL_KICK = 3
 NB_FLAG_EXCLUDE_SELF = 1
 NB_FLAG_UNIFORM_MASS = 2
+NB_INIT_UNIFORM_CUBE = 0
+NB_INIT_PLUMMER = 1
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -41,6 +43,7 @@ _ARGTYPES = {
     "nb_dev_drift": [_p, _p, _p, _i64, _d, _p],
     "nb_dev_kick": [_p, _p, _p, _i64, _d, _p],
     "nb_dev_energy": [_p, _p, _i64, _d, _d, _p, _p, _i64, _p],
+    "nb_dev_init": [_i, ctypes.c_uint64, _i64, _p, _p, _p],
 }
 
 _lib: Optional[ctypes.CDLL] = None

@@ -472,6 +472,25 @@ int nb_dev_energy_f64(const void* pos4, const void* vel4, int64_t n, double g, d
   return dev_energy<double>(pos4, vel4, n, g, eps2, out6, ws, ws_bytes, stream);
 }
 
+static int dev_init(int precision_bytes, int kind, uint64_t seed, int64_t n, void* pos4, void* vel4, void* stream) {
+  if (n < 1) return fail(NB_ERR_ARG, "n must be >= 1");
+  if (kind != NB_INIT_UNIFORM_CUBE && kind != NB_INIT_PLUMMER) return fail(NB_ERR_ARG, "unknown generator kind");
+  if (!pos4 || !vel4 || !aligned16(pos4) || !aligned16(vel4)) return fail(NB_ERR_ARG, "pos4/vel4 must be 16-byte aligned device pointers");
+  if (cudaError_t be = bind_device_of(pos4)) return cuda_fail(be, "pos4 is not a device pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (precision_bytes == 4)
+    NB_CUDA(launch_init<float>(kind, seed, n, static_cast<V4<float>*>(pos4), static_cast<V4<float>*>(vel4), st));
+  else
+    NB_CUDA(launch_init<double>(kind, seed, n, static_cast<V4<double>*>(pos4), static_cast<V4<double>*>(vel4), st));
+  return NB_OK;
+}
+int nb_dev_init_f32(int kind, uint64_t seed, int64_t n, void* pos4, void* vel4, void* stream) {
+  return dev_init(4, kind, seed, n, pos4, vel4, stream);
+}
+int nb_dev_init_f64(int kind, uint64_t seed, int64_t n, void* pos4, void* vel4, void* stream) {
+  return dev_init(8, kind, seed, n, pos4, vel4, stream);
+}
+
 const char* nb_last_error(void) { return t_err.c_str(); }
 const char* nb_version(void) { return "nbody_b200 0.1.0 (sm_100a)"; }
 int64_t nb_launch_count(void) { return g_launches.load(); }

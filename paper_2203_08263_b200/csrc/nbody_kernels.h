@@ -52,6 +52,9 @@ template <typename R> cudaError_t launch_pack_soa(const R* x, const R* y, const 
 template <typename R> cudaError_t launch_unpack_soa(const V4<R>* in, R* x, R* y, R* z, int64_t n, cudaStream_t s);
 template <typename R> cudaError_t launch_pack_aos(const R* xyz, const R* w, V4<R>* out, int64_t n, cudaStream_t s);
 template <typename R> cudaError_t launch_unpack_aos(const V4<R>* in, R* xyz, int64_t n, cudaStream_t s);
+// kind 0: uniform cube, 1: Plummer sphere (BASELINE.json generators).
+template <typename R> cudaError_t launch_init(int kind, unsigned long long seed, int64_t n, V4<R>* pos, V4<R>* vel,
+                                              cudaStream_t s);
 template <typename R> cudaError_t launch_energy(const V4<R>* pos, const V4<R>* vel, int64_t n, double g, double eps2,
                                                 double* out6, double* phi, cudaStream_t s);
 

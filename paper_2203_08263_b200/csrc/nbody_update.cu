@@ -199,3 +199,79 @@ NB_INST(double)
 #undef NB_INST
 
 }  // namespace nb
+
+// ---------------------------------------------------------------- on-device initial conditions
+// splitmix64 closed form (core.py:100-107): state_k = seed + k*gamma, k = 1..,
+// mapped to [0,1) as (z >> 11) * 2^-53 (core.py:110-113); all in FP64, rounded
+// once to R exactly like the host generators (core.uniform_cube / plummer_sphere).
+namespace nb {
+
+__device__ __forceinline__ double unit_draw(unsigned long long seed, unsigned long long k) {
+  unsigned long long z = seed + (k + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * 0x1.0p-53;
+}
+
+// Uniform cube (BASELINE configs 0-3): draws (ux,uy,uz,uvx,uvy,uvz,um) per body,
+// x = -1 + 2u, v = -0.1 + 0.2u, m = 0.5 + u.
+template <typename R>
+__global__ void init_cube_kernel(unsigned long long seed, int64_t n, V4<R>* pos, V4<R>* vel) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = 7ull * (unsigned long long)i;
+    V4<R> p, v;
+    p.x = (R)__dadd_rn(-1.0, __dmul_rn(2.0, unit_draw(seed, k)));
+    p.y = (R)__dadd_rn(-1.0, __dmul_rn(2.0, unit_draw(seed, k + 1)));
+    p.z = (R)__dadd_rn(-1.0, __dmul_rn(2.0, unit_draw(seed, k + 2)));
+    v.x = (R)__dadd_rn(-0.1, __dmul_rn(0.2, unit_draw(seed, k + 3)));
+    v.y = (R)__dadd_rn(-0.1, __dmul_rn(0.2, unit_draw(seed, k + 4)));
+    v.z = (R)__dadd_rn(-0.1, __dmul_rn(0.2, unit_draw(seed, k + 5)));
+    p.w = (R)__dadd_rn(0.5, unit_draw(seed, k + 6));
+    v.w = R(0);
+    st4(pos + i, p);
+    st4(vel + i, v);
+  }
+}
+
+// Plummer sphere (BASELINE config 4): draws (ur,uc,uphi); r = (ur^(-2/3)-1)^(-1/2),
+// cos(theta) = 2uc - 1, phi = 2 pi uphi, v = 0, m = 1/N.
+template <typename R>
+__global__ void init_plummer_kernel(unsigned long long seed, int64_t n, V4<R>* pos, V4<R>* vel) {
+  const double two_pi = 6.283185307179586;
+  const double m = 1.0 / (double)n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = 3ull * (unsigned long long)i;
+    double ur = unit_draw(seed, k);
+    ur = ur > 0x1.0p-53 ? ur : 0x1.0p-53;
+    const double r = 1.0 / sqrt(pow(ur, -2.0 / 3.0) - 1.0);
+    const double ct = __dsub_rn(__dmul_rn(2.0, unit_draw(seed, k + 1)), 1.0);
+    const double st = sqrt(fmax(0.0, __dsub_rn(1.0, __dmul_rn(ct, ct))));
+    const double phi = __dmul_rn(two_pi, unit_draw(seed, k + 2));
+    double sp, cp;
+    sincos(phi, &sp, &cp);
+    V4<R> p, v;
+    p.x = (R)__dmul_rn(__dmul_rn(r, st), cp);
+    p.y = (R)__dmul_rn(__dmul_rn(r, st), sp);
+    p.z = (R)__dmul_rn(r, ct);
+    p.w = (R)m;
+    v.x = v.y = v.z = v.w = R(0);
+    st4(pos + i, p);
+    st4(vel + i, v);
+  }
+}
+
+template <typename R>
+cudaError_t launch_init(int kind, unsigned long long seed, int64_t n, V4<R>* pos, V4<R>* vel, cudaStream_t s) {
+  const int blocks = blocks_for(n, 256);
+  if (kind == 0)
+    init_cube_kernel<R><<<blocks, 256, 0, s>>>(seed, n, pos, vel);
+  else
+    init_plummer_kernel<R><<<blocks, 256, 0, s>>>(seed, n, pos, vel);
+  count_launch();
+  return cudaGetLastError();
+}
+template cudaError_t launch_init<float>(int, unsigned long long, int64_t, V4<float>*, V4<float>*, cudaStream_t);
+template cudaError_t launch_init<double>(int, unsigned long long, int64_t, V4<double>*, V4<double>*, cudaStream_t);
+
+}  // namespace nb

@@ -106,6 +106,40 @@ class DeviceState:
         self.cur_is_a = True
         self._host_keepalive = (host_pos, host_vel)
 
+    @classmethod
+    def from_generator(cls, kind: str, n: int, seed: int, dtype,
+                       device: Optional[torch.device] = None) -> "DeviceState":
+        """A resident system generated on the device (nb_dev_init): ``kind`` is
+        "uniform_cube" or "plummer_sphere", the BASELINE.json generators of
+        ``core`` -- no host generation and no H2D copy of the state."""
+        codes = {"uniform_cube": _native.NB_INIT_UNIFORM_CUBE, "plummer_sphere": _native.NB_INIT_PLUMMER}
+        if kind not in codes:
+            raise ValueError(f"unknown generator {kind!r}")
+        dtype = np.dtype(dtype)
+        self = cls.__new__(cls)
+        self.dtype = dtype
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.n, self.i_begin, self.n_i = int(n), 0, int(n)
+        self.sfx = "_f32" if dtype == np.float32 else "_f64"
+        self.pbytes = dtype.itemsize
+        tdt = TORCH_DTYPE[dtype]
+        self.pos_a = torch.empty((self.n, 4), dtype=tdt, device=self.device)
+        self.pos_b = torch.empty_like(self.pos_a)
+        self.vel = torch.empty((self.n, 4), dtype=tdt, device=self.device)
+        _native.call("nb_dev_init" + self.sfx, codes[kind], int(seed), self.n, self.pos_a.data_ptr(),
+                     self.vel.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
+        self.masses = None  # device-resident only; see masses_host()
+        self.acc = torch.zeros((self.n, 4), dtype=tdt, device=self.device)
+        self.carry = torch.zeros((3, self.n), dtype=torch.float64, device=self.device)
+        self.ws_bytes = _native.workspace_bytes(self.pbytes, self.n)
+        self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.cur_is_a = True
+        self._host_keepalive = ()
+        return self
+
+    def masses_host(self) -> np.ndarray:
+        return self.pos_cur[:, 3].cpu().numpy()
+
     # -------------------------------------------------------------- buffers
     @property
     def pos_cur(self) -> torch.Tensor:

@@ -436,6 +436,28 @@ def test_uniform_mass_path_matches_general_path(prec, oracle):
     assert nb_accel_dev(a_uni, a_gen) <= (1e-14 if prec == "double" else 2e-6)
 
 
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_device_generators_match_host(prec):
+    """nb_dev_init: the uniform cube is bit-identical to core.uniform_cube; the
+    Plummer sphere (libm pow/sincos on the device) agrees to <= 2 ulp."""
+    from paper_2203_08263_b200.device import DeviceState
+    n = 100003
+    dtype = np.dtype(np.float32 if prec == "single" else np.float64)
+    st = DeviceState.from_generator("uniform_cube", n, 7, dtype)
+    host = nb.uniform_cube(n, 7, nb.Precision(prec))
+    np.testing.assert_array_equal(st.positions_host(), host.position_matrix().astype(dtype))
+    np.testing.assert_array_equal(st.velocities_host(), np.stack(host.velocities, 1))
+    np.testing.assert_array_equal(st.masses_host(), host.masses)
+    pl = DeviceState.from_generator("plummer_sphere", n, 7, dtype)
+    hp = nb.plummer_sphere(n, 7, nb.Precision(prec))
+    got, want = pl.positions_host().astype(np.float64), hp.position_matrix()
+    # component errors measured in ulps of the body's radius (a component near 0
+    # inherits the absolute error of cos/sin, not a relative one)
+    ulp = np.spacing(np.linalg.norm(want, axis=1).astype(dtype)).astype(np.float64)[:, None]
+    assert np.max(np.abs(got - want) / ulp) <= 4.0
+    np.testing.assert_array_equal(pl.masses_host(), hp.masses)
+
+
 # --------------------------------------------------------------------------- plugin + diagnostics
 
 @pytest.mark.parametrize("prec", ["double", "single"])
