@@ -144,6 +144,23 @@ int nb_dev_step_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_
                     void* vel4, void* pos4_next, void* workspace, int64_t workspace_bytes,
                     void* stream);
 
+/* nb_dev_step_* with a fused NVLink peer-store epilogue (multi-GPU without an
+ * all-gather): drift modes also store each drifted row into every buffer of
+ * peer_pos4_next[0..n_peers) (up to 8 UVA pointers to the next-position buffers
+ * of the other GPUs, e.g. from CUDA IPC / symmetric memory) and end with a
+ * system-scope fence.  The caller orders steps across GPUs with a barrier
+ * between the local-source pass and the remote-source pass of the next step. */
+int nb_dev_step_p2p_f32(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i,
+                        int64_t j_begin, int64_t j_count, double g, double eps2, double dt,
+                        int mode, int flags, double* carry, int carry_mode, void* acc4,
+                        void* vel4, void* pos4_next, void* const* peer_pos4_next, int n_peers,
+                        void* workspace, int64_t workspace_bytes, void* stream);
+int nb_dev_step_p2p_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i,
+                        int64_t j_begin, int64_t j_count, double g, double eps2, double dt,
+                        int mode, int flags, double* carry, int carry_mode, void* acc4,
+                        void* vel4, void* pos4_next, void* const* peer_pos4_next, int n_peers,
+                        void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Device-resident kernels.simulate for one GPU: `steps` fused steps plus the final
  * evaluation and kick (steps+1 launches), ping-ponging pos4_a <-> pos4_b.  On
  * return (stream-ordered) the final positions are in pos4_a if steps is even,

@@ -37,6 +37,8 @@ _ARGTYPES = {
     "nb_host_step_aos": [_p] * 5 + [_i64, _d],
     "nb_host_simulate_soa": [_p] * 7 + [_i64, _d, _d, _d, _i64],
     "nb_dev_step": [_p, _i64, _i64, _i64, _i64, _i64, _d, _d, _d, _i, _i, _p, _i, _p, _p, _p, _p, _i64, _p],
+    "nb_dev_step_p2p": [_p, _i64, _i64, _i64, _i64, _i64, _d, _d, _d, _i, _i, _p, _i, _p, _p, _p, _p, _i, _p,
+                        _i64, _p],
     "nb_dev_simulate": [_p, _p, _p, _p, _i64, _d, _d, _d, _i64, _i, _p, _i64, _p, ctypes.POINTER(_i)],
     "nb_dev_simulate_timed": [_p, _p, _p, _p, _i64, _d, _d, _d, _i64, _i, _p, _i64, _p, ctypes.POINTER(_i),
                               ctypes.POINTER(ctypes.c_float)],

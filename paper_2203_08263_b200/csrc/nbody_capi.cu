@@ -58,7 +58,8 @@ template <typename R>
 int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
              int64_t j_count, double g, double eps2, double dt, int mode, int flags,
              double* carry, int carry_mode, void* acc4, void* vel4, void* pos4_next,
-             void* workspace, int64_t workspace_bytes, void* stream) {
+             void* workspace, int64_t workspace_bytes, void* stream,
+             void* const* peers = nullptr, int n_peers = 0) {
   if (n_all < 1 || i_begin < 0 || n_i < 0 || i_begin + n_i > n_all)
     return fail(NB_ERR_ARG, "target range [i_begin, i_begin+n_i) must lie in [0, n_all)");
   if (j_begin < 0 || j_begin >= n_all || j_count < 0 || j_count > n_all)
@@ -68,6 +69,11 @@ int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int6
   if (carry_mode < 0 || carry_mode > 2) return fail(NB_ERR_ARG, "carry_mode must be 0, 1 or 2");
   if (carry_mode != 0 && !carry) return fail(NB_ERR_ARG, "carry buffer required for carry_mode 1/2");
   if (!(g == g) || !(eps2 >= 0.0)) return fail(NB_ERR_ARG, "g must be a number and eps2 >= 0");
+  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && !peers))
+    return fail(NB_ERR_ARG, "n_peers must be in [0, 8] with a peer pointer array");
+  for (int q = 0; q < n_peers; ++q)
+    if (!peers[q] || !aligned16(peers[q]) || peers[q] == pos4)
+      return fail(NB_ERR_ARG, "peer next-position buffers must be 16-byte aligned and must not alias pos4");
   if (n_i == 0) return NB_OK;
   if (!pos4 || !aligned16(pos4)) return fail(NB_ERR_ARG, "pos4 must be a 16-byte aligned device pointer");
   const bool finalize = carry_mode != 1;
@@ -95,6 +101,8 @@ int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int6
   a.vel = static_cast<V4<R>*>(vel4);
   a.pos_next = static_cast<V4<R>*>(pos4_next);
   a.slots = reinterpret_cast<double*>(static_cast<char*>(workspace) + counters_bytes(geo.n_iblocks));
+  a.n_peers = n_peers;
+  for (int q = 0; q < n_peers; ++q) a.peers[q] = static_cast<V4<R>*>(peers[q]);
   cudaError_t e = launch_step<R>(a, flags & (NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS),
                                  static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "launch_step");
@@ -426,6 +434,20 @@ int nb_dev_step_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_
                     void* stream) {
   return dev_step<double>(pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, flags, carry,
                           carry_mode, acc4, vel4, pos4_next, workspace, workspace_bytes, stream);
+}
+int nb_dev_step_p2p_f32(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
+                        int64_t j_count, double g, double eps2, double dt, int mode, int flags, double* carry,
+                        int carry_mode, void* acc4, void* vel4, void* pos4_next, void* const* peer_pos4_next,
+                        int n_peers, void* workspace, int64_t workspace_bytes, void* stream) {
+  return dev_step<float>(pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, flags, carry, carry_mode,
+                         acc4, vel4, pos4_next, workspace, workspace_bytes, stream, peer_pos4_next, n_peers);
+}
+int nb_dev_step_p2p_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
+                        int64_t j_count, double g, double eps2, double dt, int mode, int flags, double* carry,
+                        int carry_mode, void* acc4, void* vel4, void* pos4_next, void* const* peer_pos4_next,
+                        int n_peers, void* workspace, int64_t workspace_bytes, void* stream) {
+  return dev_step<double>(pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, flags, carry, carry_mode,
+                          acc4, vel4, pos4_next, workspace, workspace_bytes, stream, peer_pos4_next, n_peers);
 }
 int nb_dev_simulate_f32(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n, double g, double dt,
                         double eps2, int64_t steps, int flags, void* workspace, int64_t workspace_bytes,

@@ -350,6 +350,7 @@ __device__ __forceinline__ void finalize_body(const StepArgs<R>& a, int64_t il, 
       p.y = add_rn(p.y, mul_rn(add_rn(v.y, mul_rn(a.half, dvy)), a.dt));
       p.z = add_rn(p.z, mul_rn(add_rn(v.z, mul_rn(a.half, dvz)), a.dt));
       st4(a.pos_next + ig, p);
+      for (int q = 0; q < a.n_peers; ++q) st4(a.peers[q] + ig, p);  // NVLink peer stores
       v.x = add_rn(v.x, dvx);
       v.y = add_rn(v.y, dvy);
       v.z = add_rn(v.z, dvz);
@@ -483,9 +484,13 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
     }
     u += t1 - t0;
   }
+  if (a.n_peers) __threadfence_system();  // peer stores visible before the rank barrier
 }
 
 // ---------------------------------------------------------------- split i-block fixup
+template <typename R, int IB>
+__device__ __forceinline__ void fixup_body(const StepArgs<R>& a, int64_t il);
+
 // One thread per target body of a split i-block: sum the FP64 partials of the
 // contributing CTAs cf..cl in ascending order (slot 2c holds a CTA's first
 // segment, 2c+1 its last) and run the epilogue.  Bodies of i-blocks one CTA
@@ -495,6 +500,12 @@ __global__ void __launch_bounds__(256) fixup_kernel(const StepArgs<R> a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   const int64_t il = blockIdx.x * 256LL + threadIdx.x;
+  fixup_body<R, IB>(a, il);
+  if (a.n_peers) __threadfence_system();  // peer stores visible before the rank barrier
+}
+
+template <typename R, int IB>
+__device__ __forceinline__ void fixup_body(const StepArgs<R>& a, int64_t il) {
   if (il >= a.n_i) return;
   const Sched S{a.units, a.grid};
   const int64_t NT = a.n_tiles;
@@ -513,7 +524,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(const StepArgs<R> a) {
 }
 
 // ---------------------------------------------------------------- configurations
-// FP32: 128 threads x 8 bodies (4 FFMA2 pairs) = 1024-body i-blocks, 256-body tiles.
+// FP32: 128 threads x 6 bodies (3 FFMA2 pairs) = 768-body i-blocks, 256-body tiles.
 // FP64: 128 threads x 4 bodies = 512-body i-blocks, 128-body tiles.
 template <bool M, bool U> struct CoreF32M : CoreF32<NB_F32_K, M, NB_F32_UNROLL, U> {
   static constexpr bool MASK_SELF = M;

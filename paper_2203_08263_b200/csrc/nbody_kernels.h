@@ -15,6 +15,8 @@ enum : int {
   NB_STEP_MODE_FINAL = 3,
 };
 
+constexpr int kMaxPeers = 8;
+
 template <typename R>
 struct StepArgs {
   const V4<R>* pos;  // n_all packed (x,y,z,m): read-only during the launch
@@ -31,6 +33,10 @@ struct StepArgs {
   double* slots;     // stream-K partial slots (workspace)
   int64_t units, n_tiles, n_iblocks;
   int64_t grid;
+  // Multi-GPU peer-store epilogue: the drifted rows are also stored straight
+  // into every peer GPU's next-position buffer over NVLink (no all-gather).
+  V4<R>* peers[kMaxPeers];
+  int n_peers;
 };
 
 struct StepGeometry {

@@ -77,7 +77,7 @@ class DeviceState:
 
     def __init__(self, positions: np.ndarray, velocities: np.ndarray, masses: np.ndarray, dtype,
                  device: Optional[torch.device] = None, i_begin: int = 0, n_i: Optional[int] = None,
-                 eps2_hint: Optional[float] = None):
+                 pos_buffer: Optional[torch.Tensor] = None):
         self.dtype = np.dtype(dtype)
         if self.dtype not in TORCH_DTYPE:
             raise ValueError(f"unsupported precision {self.dtype}")
@@ -96,8 +96,15 @@ class DeviceState:
         host_pos = pack_bodies(np.asarray(positions, self.dtype), self.masses, self.dtype, pin=True)
         host_vel = pack_bodies(np.asarray(velocities, self.dtype)[self.i_begin:self.i_begin + self.n_i],
                                None, self.dtype, pin=True)
-        self.pos_a = host_pos.to(self.device, non_blocking=True)
-        self.pos_b = torch.empty_like(self.pos_a)
+        if pos_buffer is not None:
+            # caller-provided (2, N, 4) storage, e.g. symmetric memory peers can write into
+            if tuple(pos_buffer.shape) != (2, self.n, 4) or pos_buffer.dtype != tdt:
+                raise ValueError("pos_buffer must be a (2, N, 4) tensor of the system precision")
+            self.pos_a, self.pos_b = pos_buffer[0], pos_buffer[1]
+            self.pos_a.copy_(host_pos, non_blocking=True)
+        else:
+            self.pos_a = host_pos.to(self.device, non_blocking=True)
+            self.pos_b = torch.empty_like(self.pos_a)
         self.vel = host_vel.to(self.device, non_blocking=True)
         self.acc = torch.zeros((max(self.n_i, 1), 4), dtype=tdt, device=self.device)
         self.carry = torch.zeros((3, max(self.n_i, 1)), dtype=torch.float64, device=self.device)
@@ -158,18 +165,24 @@ class DeviceState:
     # -------------------------------------------------------------- kernels
     def step(self, g: float, eps2: float, dt: float, mode: int, flags: int,
              j_begin: Optional[int] = None, j_count: Optional[int] = None, carry_mode: int = 0,
-             acc_out: Optional[torch.Tensor] = None) -> None:
-        """One fused force(+update) launch on the current positions (nb_dev_step)."""
+             acc_out: Optional[torch.Tensor] = None, peers: Optional[list] = None) -> None:
+        """One fused force(+update) launch on the current positions (nb_dev_step).
+        ``peers``: device pointers of other GPUs' next-position buffers; the drifted
+        rows are then also stored there by the kernel (nb_dev_step_p2p)."""
         j_begin = self.i_begin if j_begin is None else j_begin
         j_count = self.n if j_count is None else j_count
         acc = self.acc if acc_out is None else acc_out
         drift = mode in (NB_STEP_FIRST, NB_STEP_KICK_DRIFT)
-        _native.call("nb_dev_step" + self.sfx, self.pos_cur.data_ptr(), self.n, self.i_begin, self.n_i,
-                     j_begin % self.n, j_count, g, eps2, dt, mode, int(flags),
-                     self.carry.data_ptr() if carry_mode else None, carry_mode, acc.data_ptr(),
-                     self.vel.data_ptr() if mode != NB_MODE_ACCEL else None,
-                     self.pos_next.data_ptr() if drift else None,
-                     self.ws.data_ptr(), self.ws_bytes, self.stream_ptr())
+        args = [self.pos_cur.data_ptr(), self.n, self.i_begin, self.n_i, j_begin % self.n, j_count, g, eps2,
+                dt, mode, int(flags), self.carry.data_ptr() if carry_mode else None, carry_mode,
+                acc.data_ptr(), self.vel.data_ptr() if mode != NB_MODE_ACCEL else None,
+                self.pos_next.data_ptr() if drift else None]
+        if peers:
+            arr = (ctypes.c_void_p * len(peers))(*peers)
+            _native.call("nb_dev_step_p2p" + self.sfx, *args, arr, len(peers), self.ws.data_ptr(),
+                         self.ws_bytes, self.stream_ptr())
+        else:
+            _native.call("nb_dev_step" + self.sfx, *args, self.ws.data_ptr(), self.ws_bytes, self.stream_ptr())
 
     def simulate(self, g: float, dt: float, eps2: float, steps: int, flags: int) -> None:
         """Whole single-device velocity-Verlet run (nb_dev_simulate): steps+1 launches."""

@@ -84,6 +84,33 @@ def run_sharded(state, g: float, dt: float, eps2: float, steps: int, flags: int,
         pending.wait()
 
 
+def run_sharded_p2p(state, g: float, dt: float, eps2: float, steps: int, flags: int,
+                    peer_next: Callable, barrier: Callable) -> None:
+    """The same loop with the exchange fused into the force kernel: the epilogue
+    of the remote-source pass stores each drifted row into every peer GPU's
+    next-position buffer over NVLink (nb_dev_step_p2p); no all-gather.
+
+    ``peer_next(cur_is_a)`` returns the peers' next-buffer pointers for the current
+    ping-pong parity; ``barrier()`` is a stream-ordered barrier over all ranks.
+    Ordering: step s sums its local sources, then barrier(s) -- every rank has
+    finished step s-1, so (RAW) all rows of p_s have landed and (WAR) nobody still
+    reads the p_{s-1} buffer the step-s epilogue now overwrites -- then the remote
+    sources and the peer-store epilogue."""
+    n, i0, ni = state.n, state.i_begin, state.n_i
+    barrier()  # every rank's buffers exist (after rendezvous / upload)
+    for s in range(steps + 1):
+        mode = NB_STEP_FIRST if s == 0 else (NB_STEP_KICK_DRIFT if s < steps else NB_STEP_FINAL_KICK)
+        state.step(g, eps2, dt, mode, flags, j_begin=i0, j_count=ni, carry_mode=1)
+        if s > 0:
+            barrier()
+        peers = peer_next(state.cur_is_a) if mode != NB_STEP_FINAL_KICK else None
+        state.step(g, eps2, dt, mode, flags, j_begin=(i0 + ni) % n, j_count=n - ni, carry_mode=2,
+                   peers=peers)
+        if mode != NB_STEP_FINAL_KICK:
+            state.swap()
+    barrier()
+
+
 def _torch_allgather(group):
     import torch.distributed as dist
 
@@ -92,12 +119,48 @@ def _torch_allgather(group):
     return gather
 
 
+def _p2p_setup(pos, vel, m, dtype, i0, ni, group):
+    """Positions in symmetric memory (CUDA IPC-mapped on every peer) and the
+    symmetric-memory device barrier."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+
+    from .device import TORCH_DTYPE, DeviceState
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if world - 1 > 8:
+        raise ValueError("the peer-store epilogue supports up to 9 GPUs")
+    if group is None:
+        group = dist.group.WORLD
+    try:
+        symm_mem.enable_symm_mem_for_group(group.group_name)
+    except (AttributeError, RuntimeError):
+        pass
+    n = pos.shape[0]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    buf = symm_mem.empty((2, n, 4), dtype=TORCH_DTYPE[np.dtype(dtype)], device=dev)
+    hdl = symm_mem.rendezvous(buf, group.group_name)
+    state = DeviceState(pos, vel, m, dtype, i_begin=i0, n_i=ni, pos_buffer=buf)
+    half = n * 4 * np.dtype(dtype).itemsize
+    peers = [q for q in range(world) if q != rank]
+    ptrs = list(hdl.buffer_ptrs)
+
+    def peer_next(cur_is_a: bool):
+        return [ptrs[q] + (half if cur_is_a else 0) for q in peers]
+
+    def barrier():
+        hdl.barrier(channel=0)
+    return state, peer_next, barrier
+
+
 def simulate_sharded(positions: np.ndarray, velocities: np.ndarray, masses: np.ndarray, dtype,
                      g: float, dt: float, eps2: float, steps: int, group=None,
-                     flags: Optional[int] = None) -> Tuple[np.ndarray, np.ndarray]:
+                     flags: Optional[int] = None, transport: str = "nccl") -> Tuple[np.ndarray, np.ndarray]:
     """Multi-GPU simulate: every rank passes the full initial state and gets the
     full final (positions, velocities) back.  Uses the default process group
-    (NCCL, one process per GPU) unless ``group`` is given."""
+    (NCCL, one process per GPU) unless ``group`` is given.  ``transport``:
+    "nccl" (in-place all-gather overlapped with the local-source pass) or "p2p"
+    (peer-store epilogue into symmetric-memory buffers; see run_sharded_p2p)."""
     import torch
     import torch.distributed as dist
 
@@ -115,8 +178,14 @@ def simulate_sharded(positions: np.ndarray, velocities: np.ndarray, masses: np.n
         # uniform masses only if no massless padding was added
         flags = kernel_flags(m, eps2, dtype) & ~NB_FLAG_EXCLUDE_SELF
         flags |= NB_FLAG_EXCLUDE_SELF if needs_self_mask(m[:n], eps2, dtype) else 0
-    state = DeviceState(pos, vel, m, dtype, i_begin=i0, n_i=ni)
-    run_sharded(state, g, dt, eps2, steps, flags, _torch_allgather(group), world)
+    if transport == "p2p":
+        state, peer_next, barrier = _p2p_setup(pos, vel, m, dtype, i0, ni, group)
+        run_sharded_p2p(state, g, dt, eps2, steps, flags, peer_next, barrier)
+    elif transport == "nccl":
+        state = DeviceState(pos, vel, m, dtype, i_begin=i0, n_i=ni)
+        run_sharded(state, g, dt, eps2, steps, flags, _torch_allgather(group), world)
+    else:
+        raise ValueError(f"unknown transport {transport!r} (expected 'nccl' or 'p2p')")
     vel_full = torch.empty((npad, 4), dtype=state.vel.dtype, device=state.device)
     dist.all_gather_into_tensor(vel_full, state.vel[:ni].contiguous(), group=group)
     out_pos = state.pos_cur[:n, :3].cpu().numpy()

@@ -19,6 +19,9 @@ from paper_2203_08263_b200.core import uniform_cube
 
 pytestmark = pytest.mark.gpu
 
+import os
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 F64_ACC_TOL = 1e-12
 F32_ACC_TOL = 1e-5
 F64_POS_TOL = 1e-12
@@ -456,6 +459,71 @@ def test_device_generators_match_host(prec):
     ulp = np.spacing(np.linalg.norm(want, axis=1).astype(dtype)).astype(np.float64)[:, None]
     assert np.max(np.abs(got - want) / ulp) <= 4.0
     np.testing.assert_array_equal(pl.masses_host(), hp.masses)
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_store_epilogue_on_one_gpu(prec, world):
+    """nb_dev_step_p2p: P emulated ranks on one device in lock step; each rank's
+    remote-source pass stores its drifted rows straight into every other rank's
+    next-position buffer (the fused exchange; no all-gather).  Sequential launches
+    on one stream stand in for the cross-GPU barrier."""
+    from paper_2203_08263_b200.device import DeviceState, kernel_flags
+    from paper_2203_08263_b200.sharded import pad_system, shard_range
+    from paper_2203_08263_b200._native import NB_STEP_FIRST, NB_STEP_KICK_DRIFT, NB_STEP_FINAL_KICK
+    from oracle.oracle import position_dev
+    s = cube(2500, 33, prec)
+    p = nb.SimParams(1.0, 1e-3, 1e-3, 4)
+    ref = nb.simulate(s, p)
+    dtype = s.precision.dtype
+    pos, vel, m = pad_system(s.position_matrix().astype(dtype), np.stack(s.velocities, 1), s.masses, world)
+    npad = pos.shape[0]
+    ranks = [DeviceState(pos, vel, m, dtype, i_begin=shard_range(npad, r, world)[0],
+                         n_i=shard_range(npad, r, world)[1]) for r in range(world)]
+    flags = kernel_flags(m, p.softening_sq, dtype)
+    for step in range(p.steps + 1):
+        mode = NB_STEP_FIRST if step == 0 else (NB_STEP_KICK_DRIFT if step < p.steps else NB_STEP_FINAL_KICK)
+        for st in ranks:
+            st.step(1.0, p.softening_sq, p.dt, mode, flags, j_begin=st.i_begin, j_count=st.n_i, carry_mode=1)
+        for st in ranks:
+            peers = None if mode == NB_STEP_FINAL_KICK else [q.pos_next.data_ptr() for q in ranks if q is not st]
+            st.step(1.0, p.softening_sq, p.dt, mode, flags, j_begin=(st.i_begin + st.n_i) % npad,
+                    j_count=npad - st.n_i, carry_mode=2, peers=peers)
+        if mode != NB_STEP_FINAL_KICK:
+            for st in ranks:
+                st.swap()
+    tol = 1e-13 if prec == "double" else 1e-6
+    for st in ranks:  # every rank holds every row
+        got = st.pos_cur[: s.count, :3].cpu().numpy().astype(np.float64)
+        assert position_dev(got, ref.position_matrix()) <= tol
+
+
+def test_symmetric_memory_p2p_path_single_rank(tmp_path):
+    """The symmetric-memory plumbing of transport="p2p" (allocation, rendezvous,
+    device barrier) on a 1-rank NCCL group, in a subprocess."""
+    import subprocess, sys, textwrap, socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    script = textwrap.dedent(f"""
+        import os, sys, numpy as np, torch, torch.distributed as dist
+        sys.path.insert(0, {REPO!r})
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="{port}", RANK="0", WORLD_SIZE="1")
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+        import paper_2203_08263_b200 as nb
+        from paper_2203_08263_b200.sharded import simulate_sharded
+        s = nb.uniform_cube(3000, 5, nb.Precision.SINGLE)
+        pos, vel = simulate_sharded(s.position_matrix().astype(np.float32), np.stack(s.velocities, 1),
+                                    s.masses, np.float32, 1.0, 1e-3, 1e-3, 3, transport="p2p")
+        ref = nb.simulate(s, nb.SimParams(1.0, 1e-3, 1e-3, 3)).position_matrix()
+        err = float(np.max(np.abs(pos - ref)))
+        dist.destroy_process_group()
+        print("ERR", err)
+        assert err <= 1e-6, err
+    """)
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
 
 
 # --------------------------------------------------------------------------- plugin + diagnostics
