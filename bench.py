@@ -197,7 +197,12 @@ def run_ours(args) -> dict:
     i0, ni = shard_range(npad, rank, world)
     mask = kernel_flags(m, cfg.softening_sq, dtype) & ~1
     mask |= 1 if needs_self_mask(m0, cfg.softening_sq, dtype) else 0
-    state = DeviceState(pos, vel, m, dtype, device=dev, i_begin=i0, n_i=ni)
+    p2p = world > 1 and args.transport == "p2p"
+    if p2p:
+        from paper_2203_08263_b200.sharded import _p2p_setup, run_sharded_p2p
+        state, peer_next, p2p_barrier = _p2p_setup(pos, vel, m, dtype, i0, ni, None)
+    else:
+        state = DeviceState(pos, vel, m, dtype, device=dev, i_begin=i0, n_i=ni)
     pristine_pos = state.pos_a.clone()
     pristine_vel = state.vel.clone()
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -222,6 +227,10 @@ def run_ours(args) -> dict:
                 launch_ms_all.append(ms)
                 return sum(ms)
             state.simulate(g, dt, eps2, steps, mask)
+            return None
+
+        if p2p:
+            run_sharded_p2p(state, g, dt, eps2, steps, mask, peer_next, p2p_barrier)
             return None
 
         def gather(full, local_rows):
@@ -332,7 +341,7 @@ def run_ours(args) -> dict:
         "config": {"workload": cfg.name, "n_bodies": cfg.n, "integrator_steps": steps,
                    "force_evaluations_per_step": steps + 1, "softening_sq": cfg.softening_sq,
                    "dt": cfg.dt, "distribution": cfg.generator.__name__,
-                   "parallelism": f"i-shard x{world}" if world > 1 else "1 GPU",
+                   "parallelism": f"i-shard x{world} ({args.transport})" if world > 1 else "1 GPU",
                    "l2": "flushed (256 MB write) between timed steps"},
         "gflops_20": FLOP_PER_INTERACTION * value / 1e9,
         "gflops_reference_convention": FLOP_PER_INTERACTION * float(cfg.n) * cfg.n * steps * args.steps
@@ -402,6 +411,8 @@ def main(argv=None):
     ap.add_argument("--config", default="C3-f32",
                     choices=["C1", "C2", "C3-f32", "C3-f64", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 position exchange: NCCL all-gather (default) or the fused peer-store epilogue")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
