@@ -36,13 +36,13 @@
 #define NB_F32_K 6
 #endif
 #ifndef NB_F32_T
-#define NB_F32_T 128
+#define NB_F32_T 64
 #endif
 #ifndef NB_F32_TJ
 #define NB_F32_TJ 256
 #endif
 #ifndef NB_F32_MINB
-#define NB_F32_MINB 3
+#define NB_F32_MINB 6
 #endif
 #ifndef NB_F32_UNROLL
 #define NB_F32_UNROLL 8
@@ -51,7 +51,7 @@
 #define NB_F32_PIPE 0
 #endif
 #ifndef NB_CHUNK
-#define NB_CHUNK 32
+#define NB_CHUNK 16
 #endif
 #ifndef NB_F64_K
 #define NB_F64_K 4

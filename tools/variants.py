@@ -14,12 +14,9 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "t64": {"NB_F32_T": 64, "NB_F32_MINB": 6},
-    "k4_t64": {"NB_F32_K": 4, "NB_F32_T": 64, "NB_F32_MINB": 8},
-    "k4": {"NB_F32_K": 4},
-    "ch64": {"NB_CHUNK": 64},
-    "tj128_ch32": {"NB_F32_TJ": 128},
-    "k6_minb4": {"NB_F32_MINB": 4},
+    "ch16": {"NB_CHUNK": 16},
+    "ch8": {"NB_CHUNK": 8},
+    "t64_ch16": {"NB_F32_T": 64, "NB_F32_MINB": 6, "NB_CHUNK": 16},
 }
 
 
