@@ -36,16 +36,16 @@
 #define NB_F32_K 6
 #endif
 #ifndef NB_F32_T
-#define NB_F32_T 64
+#define NB_F32_T 256
 #endif
 #ifndef NB_F32_TJ
 #define NB_F32_TJ 256
 #endif
 #ifndef NB_F32_MINB
-#define NB_F32_MINB 6
+#define NB_F32_MINB 1
 #endif
 #ifndef NB_F32_UNROLL
-#define NB_F32_UNROLL 8
+#define NB_F32_UNROLL 16
 #endif
 #ifndef NB_F32_PIPE
 #define NB_F32_PIPE 0
@@ -66,7 +66,7 @@
 #define NB_F64_MINB 3
 #endif
 #ifndef NB_F64_UNROLL
-#define NB_F64_UNROLL 4
+#define NB_F64_UNROLL 8
 #endif
 
 
@@ -152,33 +152,49 @@ struct CoreF32 {
 #pragma unroll
     for (int q = 0; q < KP; ++q) tx[q] = ty[q] = tz[q] = 0ull;
   }
+  // One source body against the K targets.  Written stage-wise across the KP
+  // pairs with w in the first operand slot of the accumulating FFMA2s: the
+  // measured best source form (tools/loop_bench.cu, +1.2 % over a per-pair
+  // order): consecutive instructions share the broadcast source operand, and the
+  // accumulate -- the instruction with three distinct register pairs, which the
+  // register file cannot feed at full rate -- gets the most reuse.
   __device__ __forceinline__ void interact(const F4& pj, int jj) {
     const f2x xj = pk(pj.x, pj.x), yj = pk(pj.y, pj.y), zj = pk(pj.z, pj.z), mj = pk(pj.w, pj.w);
+    f2x dx[KP], dy[KP], dz[KP], d2[KP], w[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) dx[q] = add2(xj, nx[q]);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) dy[q] = add2(yj, ny[q]);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) dz[q] = add2(zj, nz[q]);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) d2[q] = fma2(dx[q], dx[q], e2);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) d2[q] = fma2(dy[q], dy[q], d2[q]);
+#pragma unroll
+    for (int q = 0; q < KP; ++q) d2[q] = fma2(dz[q], dz[q], d2[q]);
 #pragma unroll
     for (int q = 0; q < KP; ++q) {
-      const f2x dx = add2(xj, nx[q]);
-      const f2x dy = add2(yj, ny[q]);
-      const f2x dz = add2(zj, nz[q]);
-      f2x d2 = fma2(dx, dx, e2);
-      d2 = fma2(dy, dy, d2);
-      d2 = fma2(dz, dz, d2);
       float d2a, d2b;
-      upk(d2, d2a, d2b);
+      upk(d2[q], d2a, d2b);
       const f2x r = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
       const f2x r2 = mul2(r, r);
       // UNI (all masses equal): m is applied once to the finished sum, saving
       // one FMUL2 of 12 per interaction pair.
-      f2x w = UNI ? mul2(r2, r) : mul2(mul2(r, mj), r2);
+      w[q] = UNI ? mul2(r2, r) : mul2(mul2(r, mj), r2);
       if (MASK) {
         float wa, wb;
-        upk(w, wa, wb);
+        upk(w[q], wa, wb);
         if (jj == selfj[2 * q]) wa = 0.f;
         if (jj == selfj[2 * q + 1]) wb = 0.f;
-        w = pk(wa, wb);
+        w[q] = pk(wa, wb);
       }
-      tx[q] = fma2(dx, w, tx[q]);
-      ty[q] = fma2(dy, w, ty[q]);
-      tz[q] = fma2(dz, w, tz[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      tx[q] = fma2(w[q], dx[q], tx[q]);
+      ty[q] = fma2(w[q], dy[q], ty[q]);
+      tz[q] = fma2(w[q], dz[q], tz[q]);
     }
   }
   // Stage A of a source body: separations, d2 and the MUFU.RSQ pair.

@@ -14,9 +14,11 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "ch16": {"NB_CHUNK": 16},
-    "ch8": {"NB_CHUNK": 8},
-    "t64_ch16": {"NB_F32_T": 64, "NB_F32_MINB": 6, "NB_CHUNK": 16},
+    "f64_t256": {"NB_F64_T": 256, "NB_F64_MINB": 1},
+    "f64_t256_k6": {"NB_F64_T": 256, "NB_F64_MINB": 1, "NB_F64_K": 6},
+    "f64_t256_u8": {"NB_F64_T": 256, "NB_F64_MINB": 1, "NB_F64_UNROLL": 8},
+    "f64_t64_minb6": {"NB_F64_T": 64, "NB_F64_MINB": 6},
+    "f64_t128_u8": {"NB_F64_UNROLL": 8},
 }
 
 
