@@ -29,17 +29,21 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB, objdir: str = OBJ) -> str:
+    """Compile the sources for sm_100a and link ``lib``; ``defines`` (e.g.
+    ["NB_CHECK"]) produce a variant build in its own ``objdir``."""
+    OBJ_ = objdir
+    os.makedirs(OBJ_, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     headers.append(os.path.join(REPO, "include", "nbody_b200.h"))
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        o = os.path.join(OBJ_, src.replace(".cu", ".o"))
         if force or _stale(o, [s] + headers):
-            cmd = [NVCC, *ARCH, *FLAGS, "-Xptxas", "-v", "-c", s, "-o", o] if verbose else \
-                  [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+            dflags = [f"-D{d}" for d in defines]
+            cmd = [NVCC, *ARCH, *FLAGS, *dflags, "-Xptxas", "-v", "-c", s, "-o", o] if verbose else \
+                  [NVCC, *ARCH, *FLAGS, *dflags, "-c", s, "-o", o]
             jobs.append(cmd)
 
     def run(cmd):
@@ -52,14 +56,23 @@ def build(verbose: bool = False, force: bool = False) -> str:
         for log in ex.map(run, jobs):
             if verbose and log:
                 sys.stderr.write(log)
-    objs = [os.path.join(OBJ, s.replace(".cu", ".o")) for s in SOURCES]
-    if force or jobs or _stale(LIB, objs):
-        link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+    objs = [os.path.join(OBJ_, s.replace(".cu", ".o")) for s in SOURCES]
+    if force or jobs or _stale(lib, objs):
+        link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs]
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(link)}\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
+
+
+def build_checked() -> str:
+    """Bounds-checked build (NB_CHECK: device traps on any out-of-range index)."""
+    return build(defines=("NB_CHECK",), lib=os.path.join(PKG, "libnbody_b200_check.so"),
+                 objdir=os.path.join(PKG, "build_check"))
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    if "--check" in sys.argv:
+        print(build_checked())
+    else:
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -13,7 +13,9 @@ import re
 from typing import Optional
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libnbody_b200.so")
+# NB_LIB_PATH selects another build of the same ABI (e.g. the bounds-checked one
+# from tools/check_build.sh); the default is the in-tree release library.
+LIB_PATH = os.environ.get("NB_LIB_PATH") or os.path.join(_PKG, "libnbody_b200.so")
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "nbody_b200.h")
 
 NB_MODE_ACCEL = 0

@@ -72,6 +72,14 @@
 
 namespace nb {
 
+// NB_CHECK builds (tools/check_build.sh) trap on any out-of-range index: the
+// stand-in for compute-sanitizer, which this pool does not offer.
+#ifdef NB_CHECK
+#define NB_DCHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define NB_DCHECK(cond) do { } while (0)
+#endif
+
 struct Sched {
   int64_t units;
   int64_t grid;
@@ -334,6 +342,7 @@ struct CoreF64 {
 template <typename R>
 __device__ __forceinline__ void finalize_body(const StepArgs<R>& a, int64_t il, double tx,
                                               double ty, double tz) {
+  NB_DCHECK(il >= 0 && il < a.n_i);
   if (a.carry_mode == 2) {
     tx = a.carry[il] + tx;
     ty = a.carry[a.n_i + il] + ty;
@@ -365,6 +374,7 @@ __device__ __forceinline__ void finalize_body(const StepArgs<R>& a, int64_t il, 
       p.x = add_rn(p.x, mul_rn(add_rn(v.x, mul_rn(a.half, dvx)), a.dt));
       p.y = add_rn(p.y, mul_rn(add_rn(v.y, mul_rn(a.half, dvy)), a.dt));
       p.z = add_rn(p.z, mul_rn(add_rn(v.z, mul_rn(a.half, dvz)), a.dt));
+      NB_DCHECK(ig >= 0 && ig < a.n_all && il >= 0 && il < a.n_i);
       st4(a.pos_next + ig, p);
       for (int q = 0; q < a.n_peers; ++q) st4(a.peers[q] + ig, p);  // NVLink peer stores
       v.x = add_rn(v.x, dvx);
@@ -426,6 +436,7 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
         if (off < s1) {
           int64_t jg = a.j_begin + off;
           if (jg >= a.n_all) jg -= a.n_all;
+          NB_DCHECK(jg >= 0 && jg < a.n_all);
           stage[r] = ld4(a.pos + jg);
         } else {
           stage[r] = B{};
@@ -490,6 +501,7 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
       // (stream-ordered after this launch) combines the contributors of the
       // i-block in ascending CTA order -- deterministic -- and runs the epilogue.
       const int64_t slot = (u == u_begin) ? 2 * c : 2 * c + 1;
+      NB_DCHECK(slot >= 0 && slot < 2 * a.grid && u >= u_begin && u < u_end);
       double* sp = a.slots + slot * 3 * IB;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -531,6 +543,7 @@ __device__ __forceinline__ void fixup_body(const StepArgs<R>& a, int64_t il) {
   int64_t sl = (S.start(cf) == b * NT) ? 2 * cf : 2 * cf + 1;
   double tx = 0.0, ty = 0.0, tz = 0.0;
   for (int64_t cc = cf; cc <= cl; ++cc, sl = 2 * cc) {
+    NB_DCHECK(sl >= 0 && sl < 2 * a.grid && cc < a.grid && o < IB);
     const double* q = a.slots + sl * 3 * IB + o;
     tx += q[0];
     ty += q[IB];

@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT
-python tools/sanitize_case.py > gpurun_out/sanitize_plain.log 2>&1 && \
-timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_case.py > gpurun_out/sanitize_memcheck.log 2>&1
-echo "memcheck rc=$?" >> gpurun_out/sanitize_memcheck.log
+NB_LIB_PATH=$PWD/paper_2203_08263_b200/libnbody_b200_check.so timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_checked.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu_checked.log
+NB_LIB_PATH=$PWD/paper_2203_08263_b200/libnbody_b200_check.so python tools/sanitize_case.py >> gpurun_out/pytest_gpu_checked.log 2>&1
