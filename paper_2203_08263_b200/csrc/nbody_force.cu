@@ -50,11 +50,14 @@
 #ifndef NB_F32_PIPE
 #define NB_F32_PIPE 0
 #endif
+#ifndef NB_F32_RCP_PAIRS
+#define NB_F32_RCP_PAIRS 0
+#endif
 #ifndef NB_CHUNK
 #define NB_CHUNK 16
 #endif
 #ifndef NB_F64_K
-#define NB_F64_K 4
+#define NB_F64_K 6
 #endif
 #ifndef NB_F64_T
 #define NB_F64_T 128
@@ -63,10 +66,13 @@
 #define NB_F64_TJ 128
 #endif
 #ifndef NB_F64_MINB
-#define NB_F64_MINB 3
+#define NB_F64_MINB 2
 #endif
 #ifndef NB_F64_UNROLL
 #define NB_F64_UNROLL 8
+#endif
+#ifndef NB_F64_STAGEWISE
+#define NB_F64_STAGEWISE 1
 #endif
 
 
@@ -186,7 +192,9 @@ struct CoreF32 {
       float d2a, d2b;
       upk(d2[q], d2a, d2b);
       const f2x r = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
-      const f2x r2 = mul2(r, r);
+      // The first NB_F32_RCP_PAIRS pairs take r^2 from MUFU.RCP instead of an
+      // FMUL2, moving work from the saturated FMA pipe to the half-idle XU pipe.
+      const f2x r2 = q < NB_F32_RCP_PAIRS ? pk(rcp_mufu(d2a), rcp_mufu(d2b)) : mul2(r, r);
       // UNI (all masses equal): m is applied once to the finished sum, saving
       // one FMUL2 of 12 per interaction pair.
       w[q] = UNI ? mul2(r2, r) : mul2(mul2(r, mj), r2);
@@ -316,6 +324,39 @@ struct CoreF64 {
     for (int jj = 0; jj < TJ; ++jj) interact(tb[jj], jj);
   }
   __device__ __forceinline__ void interact(const D4& pj, int jj) {
+#if NB_F64_STAGEWISE
+    // Stage-wise across the K targets with w in the first slot of the
+    // accumulating DFMAs (the FP32 kernel's measured best source form).
+    double dx[K], dy[K], dz[K], d2[K], w[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) dx[k] = pj.x + nx[k];
+#pragma unroll
+    for (int k = 0; k < K; ++k) dy[k] = pj.y + ny[k];
+#pragma unroll
+    for (int k = 0; k < K; ++k) dz[k] = pj.z + nz[k];
+#pragma unroll
+    for (int k = 0; k < K; ++k) d2[k] = fma(dx[k], dx[k], e2);
+#pragma unroll
+    for (int k = 0; k < K; ++k) d2[k] = fma(dy[k], dy[k], d2[k]);
+#pragma unroll
+    for (int k = 0; k < K; ++k) d2[k] = fma(dz[k], dz[k], d2[k]);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double y = rsqrt_seed(d2[k]);
+      const double t = y * y;
+      const double e = fma(-d2[k], t, 1.0);
+      const double my3 = UNI ? t * y : pj.w * (t * y);
+      const double q = e * fma(e, 1.875, 1.5);
+      w[k] = fma(my3, q, my3);
+      if (MASK && jj == selfj[k]) w[k] = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      sx[k] = fma(w[k], dx[k], sx[k]);
+      sy[k] = fma(w[k], dy[k], sy[k]);
+      sz[k] = fma(w[k], dz[k], sz[k]);
+    }
+#else
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const double dx = pj.x + nx[k], dy = pj.y + ny[k], dz = pj.z + nz[k];
@@ -335,6 +376,7 @@ struct CoreF64 {
       sy[k] = fma(dy, w, sy[k]);
       sz[k] = fma(dz, w, sz[k]);
     }
+#endif
   }
 };
 

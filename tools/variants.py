@@ -14,11 +14,9 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "f64_t256": {"NB_F64_T": 256, "NB_F64_MINB": 1},
-    "f64_t256_k6": {"NB_F64_T": 256, "NB_F64_MINB": 1, "NB_F64_K": 6},
-    "f64_t256_u8": {"NB_F64_T": 256, "NB_F64_MINB": 1, "NB_F64_UNROLL": 8},
-    "f64_t64_minb6": {"NB_F64_T": 64, "NB_F64_MINB": 6},
-    "f64_t128_u8": {"NB_F64_UNROLL": 8},
+    "rcp1": {"NB_F32_RCP_PAIRS": 1},
+    "rcp2": {"NB_F32_RCP_PAIRS": 2},
+    "rcp3": {"NB_F32_RCP_PAIRS": 3},
 }
 
 
