@@ -332,15 +332,16 @@ def test_zero_softening_excludes_self(prec, n, oracle):
     assert nb_accel_dev(a, want) <= tol
 
 
-@pytest.mark.parametrize("cfg_name", ["C2", "C3-f32", "C3-f64", "C4"])
+@pytest.mark.parametrize("cfg_name", ["C2", "C3-f32", "C3-f64", "C4", "C5"])
 def test_full_size_accelerations_row_sampled(cfg_name, oracle):
-    """BASELINE sizes: 192 rows (first, last, random) of the initial accelerations
-    against the long-double oracle."""
+    """BASELINE sizes (up to C5's 4,194,304 bodies, the maximum size): 192 rows
+    (first, last, random; 48 at C5) of the initial accelerations against the
+    long-double oracle."""
     cfg = nb.BASELINE_CONFIGS[cfg_name]
     s = cfg.system()
     a = as_mat(accel_of(s, cfg.params()))
     rng = np.random.default_rng(1)
-    rows = np.unique(np.concatenate([[0, 1, cfg.n - 1], rng.integers(0, cfg.n, 189)]))
+    rows = np.unique(np.concatenate([[0, 1, cfg.n - 1], rng.integers(0, cfg.n, 45 if cfg_name == "C5" else 189)]))
     pos = s.position_matrix()
     want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)),
                                 s.masses.astype(np.float64), rows, 1.0, cfg.softening_sq)

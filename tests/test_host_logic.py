@@ -113,3 +113,18 @@ def test_shard_arithmetic():
     assert p.shape == (12, 3) and np.all(m[10:] == 0) and np.all(np.abs(p[10:]) > 1e17)
     p2, _, _ = pad_system(pos, np.zeros((10, 3)), np.ones(10), 5)
     assert p2 is pos
+
+
+def test_empty_and_mismatched_inputs_rejected_before_device_work():
+    """Empty and ragged inputs raise ValueError like the reference's validation
+    (core.py:157-180) -- no device is touched."""
+    with pytest.raises(ValueError):
+        nb.simulate_arrays(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros(0), 1e-3, 1e-3, 1)
+    with pytest.raises(ValueError):
+        nb.simulate_arrays(np.zeros((4, 3)), np.zeros((3, 3)), np.ones(4), 1e-3, 1e-3, 1)
+    with pytest.raises(ValueError):
+        nb.simulate_arrays(np.zeros((4, 3)), np.zeros((4, 3)), np.ones(4), 1e-3, 1e-3, 0)
+    with pytest.raises(ValueError):
+        nb.simulate_arrays(np.zeros((4, 3)), np.zeros((4, 3)), np.ones(4), -1.0, 1e-3, 1)
+    with pytest.raises(ValueError):
+        nb.system_from_arrays(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros(0))
