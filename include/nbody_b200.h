@@ -108,9 +108,9 @@ int nb_host_simulate_soa_f64(double* px, double* py, double* pz, double* vx, dou
 
 /* ---------------------------------------------------------------- device (packed) */
 
-/* Workspace bytes a nb_dev_accel_* / nb_dev_step_* call needs for an i-shard of
- * n_i bodies; precision_bytes is 4 or 8.  The workspace must be zero-filled once
- * when first allocated and is left zeroed by every call (reusable). */
+/* Workspace bytes a nb_dev_step_* call needs for an i-shard of n_i bodies;
+ * precision_bytes is 4 or 8.  Scratch only (FP64 partial sums of i-blocks split
+ * between CTAs): no initialisation needed, reusable across calls on one stream. */
 int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i);
 
 /* Fused softened all-pairs force (+ optional velocity-Verlet update) for the

@@ -12,8 +12,8 @@ HBM layout (one GPU, or one i-shard of a multi-GPU run):
 * ``vel``, ``acc`` -- (n_i, 4) for the target rows only; ``acc`` holds the
   previous step's accelerations for the trapezoidal kick;
 * ``carry`` -- (3, n_i) FP64 partial sums for a split source range;
-* ``ws`` -- the stream-K workspace (arrival counters + FP64 partial slots),
-  zero-filled once and left zeroed by every launch.
+* ``ws`` -- the stream-K workspace (FP64 partial slots of split i-blocks; every
+  slot is written before it is read within a launch, so it needs no init).
 """
 
 from __future__ import annotations
@@ -91,27 +91,45 @@ class DeviceState:
         self.n_i = self.n - self.i_begin if n_i is None else int(n_i)
         self.sfx = "_f32" if self.dtype == np.float32 else "_f64"
         self.pbytes = self.dtype.itemsize
-        self.masses = np.ascontiguousarray(masses, dtype=self.dtype)
         tdt = TORCH_DTYPE[self.dtype]
-        host_pos = pack_bodies(np.asarray(positions, self.dtype), self.masses, self.dtype, pin=True)
-        host_vel = pack_bodies(np.asarray(velocities, self.dtype)[self.i_begin:self.i_begin + self.n_i],
-                               None, self.dtype, pin=True)
+        # pinned staging, reused by every load()/readback of this state
+        self._h_pos = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
+        self._h_vel = torch.empty((max(self.n_i, 1), 4), dtype=tdt, pin_memory=True)
+        self._h_out = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
+        self._h2d_done = None
         if pos_buffer is not None:
             # caller-provided (2, N, 4) storage, e.g. symmetric memory peers can write into
             if tuple(pos_buffer.shape) != (2, self.n, 4) or pos_buffer.dtype != tdt:
                 raise ValueError("pos_buffer must be a (2, N, 4) tensor of the system precision")
             self.pos_a, self.pos_b = pos_buffer[0], pos_buffer[1]
-            self.pos_a.copy_(host_pos, non_blocking=True)
         else:
-            self.pos_a = host_pos.to(self.device, non_blocking=True)
+            self.pos_a = torch.empty((self.n, 4), dtype=tdt, device=self.device)
             self.pos_b = torch.empty_like(self.pos_a)
-        self.vel = host_vel.to(self.device, non_blocking=True)
-        self.acc = torch.zeros((max(self.n_i, 1), 4), dtype=tdt, device=self.device)
-        self.carry = torch.zeros((3, max(self.n_i, 1)), dtype=torch.float64, device=self.device)
+        self.vel = torch.empty((max(self.n_i, 1), 4), dtype=tdt, device=self.device)
+        # acc, carry and the stream-K slots are always written before they are read
+        self.acc = torch.empty((max(self.n_i, 1), 4), dtype=tdt, device=self.device)
+        self.carry = torch.empty((3, max(self.n_i, 1)), dtype=torch.float64, device=self.device)
         self.ws_bytes = _native.workspace_bytes(self.pbytes, max(self.n_i, 1))
-        self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.load(positions, velocities, masses)
+
+    def load(self, positions: np.ndarray, velocities: np.ndarray, masses: np.ndarray) -> None:
+        """(Re)initialise the resident state from host arrays (pinned staging +
+        asynchronous H2D on the current stream); buffers are reused."""
+        if self._h2d_done is not None:
+            self._h2d_done.synchronize()  # staging still feeding the previous copy
+        self.masses = np.ascontiguousarray(masses, dtype=self.dtype)
+        hp = self._h_pos.numpy()
+        hp[:, :3] = positions
+        hp[:, 3] = self.masses
+        hv = self._h_vel.numpy()
+        hv[: self.n_i, :3] = np.asarray(velocities)[self.i_begin:self.i_begin + self.n_i]
+        hv[:, 3] = 0
+        self.pos_a.copy_(self._h_pos, non_blocking=True)
+        self.vel.copy_(self._h_vel, non_blocking=True)
+        self._h2d_done = torch.cuda.Event()
+        self._h2d_done.record()
         self.cur_is_a = True
-        self._host_keepalive = (host_pos, host_vel)
 
     @classmethod
     def from_generator(cls, kind: str, n: int, seed: int, dtype,
@@ -136,12 +154,15 @@ class DeviceState:
         _native.call("nb_dev_init" + self.sfx, codes[kind], int(seed), self.n, self.pos_a.data_ptr(),
                      self.vel.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
         self.masses = None  # device-resident only; see masses_host()
-        self.acc = torch.zeros((self.n, 4), dtype=tdt, device=self.device)
-        self.carry = torch.zeros((3, self.n), dtype=torch.float64, device=self.device)
+        self._h_pos = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
+        self._h_vel = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
+        self._h_out = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
+        self._h2d_done = None
+        self.acc = torch.empty((self.n, 4), dtype=tdt, device=self.device)
+        self.carry = torch.empty((3, self.n), dtype=torch.float64, device=self.device)
         self.ws_bytes = _native.workspace_bytes(self.pbytes, self.n)
-        self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.cur_is_a = True
-        self._host_keepalive = ()
         return self
 
     def masses_host(self) -> np.ndarray:
@@ -230,7 +251,10 @@ class DeviceState:
 
     # -------------------------------------------------------------- host views
     def positions_host(self) -> np.ndarray:
-        return self.pos_cur[:, :3].cpu().numpy()
+        """Current positions (N, 3): one D2H of the packed rows into pinned memory."""
+        self._h_out.copy_(self.pos_cur)
+        return np.array(self._h_out.numpy()[:, :3])
 
     def velocities_host(self) -> np.ndarray:
-        return self.vel[: self.n_i, :3].cpu().numpy()
+        self._h_out[: self.vel.shape[0]].copy_(self.vel)
+        return np.array(self._h_out.numpy()[: self.n_i, :3])

@@ -183,7 +183,7 @@ def compute_accelerations(sys_, params, variant: Optional[KernelVariant] = None,
                           out: Optional[AccelerationBuffer] = None) -> AccelerationBuffer:
     """Softened all-pairs accelerations of the current state, written into
     ``out`` (allocated if None) in the system precision; returns ``out``."""
-    from .device import DeviceState, kernel_flags
+    from .device import kernel_flags
     dtype = _dtype(sys_)
     if out is None:
         out = AccelerationBuffer.allocate(_count(sys_), _value(sys_.precision))
@@ -191,7 +191,7 @@ def compute_accelerations(sys_, params, variant: Optional[KernelVariant] = None,
     pos = _matrix(sys_, "positions")
     m = np.asarray(sys_.masses, dtype)
     eps2 = params.softening_sq
-    st = DeviceState(pos, np.zeros_like(pos), m, dtype)
+    st = _resident_state(pos, np.zeros_like(pos), m, dtype)
     a = st.accelerations(params.gravitational_constant, eps2, kernel_flags(m, eps2, dtype))
     host = a[:, :3].cpu().numpy()
     out.x[...] = host[:, 0]
@@ -226,7 +226,7 @@ def simulate_arrays(positions, velocities, masses, softening_sq: float, dt: floa
     final (N,3) positions and velocities out, in the input precision (float32 or
     float64; ``precision`` overrides).  Runs sharded over the process group when
     torch.distributed is initialised with more than one rank."""
-    from .device import DeviceState, kernel_flags
+    from .device import kernel_flags
     pos = np.asarray(positions)
     if precision is not None:
         dtype = Precision(_value(precision)).dtype
@@ -246,9 +246,29 @@ def simulate_arrays(positions, velocities, masses, softening_sq: float, dt: floa
     if _distributed_world(group) > 1:
         from .sharded import simulate_sharded
         return simulate_sharded(pos, vel, m, dtype, G, dt, softening_sq, steps, group=group)
-    st = DeviceState(pos, vel, m, dtype)
+    st = _resident_state(pos, vel, m, dtype)
     st.simulate(G, dt, softening_sq, steps, kernel_flags(m, softening_sq, dtype))
     return st.positions_host(), st.velocities_host()
+
+
+_STATE_CACHE: dict = {}
+
+
+def _resident_state(pos, vel, m, dtype):
+    """A DeviceState for (N, precision, device), reused across calls so repeated
+    simulate() calls pay only the H2D/D2H of their own data, not allocation."""
+    import torch
+
+    from .device import DeviceState
+    key = (pos.shape[0], np.dtype(dtype).str, torch.cuda.current_device())
+    st = _STATE_CACHE.get(key)
+    if st is None:
+        if len(_STATE_CACHE) >= 4:
+            _STATE_CACHE.clear()
+        st = _STATE_CACHE[key] = DeviceState(pos, vel, m, dtype)
+    else:
+        st.load(pos, vel, m)
+    return st
 
 
 def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
