@@ -86,7 +86,7 @@ class DeviceState:
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise RuntimeError("DeviceState needs a CUDA device; there is no CPU fallback")
-        self.n = int(positions.shape[0])
+        self.n = int(np.asarray(masses).shape[0])
         self.i_begin = int(i_begin)
         self.n_i = self.n - self.i_begin if n_i is None else int(n_i)
         self.sfx = "_f32" if self.dtype == np.float32 else "_f64"
@@ -113,17 +113,24 @@ class DeviceState:
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.load(positions, velocities, masses)
 
-    def load(self, positions: np.ndarray, velocities: np.ndarray, masses: np.ndarray) -> None:
-        """(Re)initialise the resident state from host arrays (pinned staging +
-        asynchronous H2D on the current stream); buffers are reused."""
+    def load(self, positions, velocities, masses: np.ndarray) -> None:
+        """(Re)initialise the resident state from host data -- (N,3) arrays or
+        (x, y, z) column tuples -- through the pinned staging and an asynchronous
+        H2D on the current stream; buffers are reused."""
         if self._h2d_done is not None:
             self._h2d_done.synchronize()  # staging still feeding the previous copy
         self.masses = np.ascontiguousarray(masses, dtype=self.dtype)
         hp = self._h_pos.numpy()
-        hp[:, :3] = positions
-        hp[:, 3] = self.masses
         hv = self._h_vel.numpy()
-        hv[: self.n_i, :3] = np.asarray(velocities)[self.i_begin:self.i_begin + self.n_i]
+        lo, hi = self.i_begin, self.i_begin + self.n_i
+        if isinstance(positions, (tuple, list)):
+            for k in range(3):
+                hp[:, k] = positions[k]
+                hv[: self.n_i, k] = velocities[k][lo:hi]
+        else:
+            hp[:, :3] = positions
+            hv[: self.n_i, :3] = np.asarray(velocities)[lo:hi]
+        hp[:, 3] = self.masses
         hv[:, 3] = 0
         self.pos_a.copy_(self._h_pos, non_blocking=True)
         self.vel.copy_(self._h_vel, non_blocking=True)
@@ -250,6 +257,19 @@ class DeviceState:
         return float(v[0]), float(v[1]), (float(v[2]), float(v[3]), float(v[4]))
 
     # -------------------------------------------------------------- host views
+    def positions_packed(self) -> np.ndarray:
+        """(N, 4) pinned view of the current positions (x, y, z, m); valid until
+        the next readback of this state."""
+        self._h_out.copy_(self.pos_cur)
+        return self._h_out.numpy()
+
+    def velocities_packed(self) -> np.ndarray:
+        h = self._h_vel_out if hasattr(self, "_h_vel_out") else None
+        if h is None:
+            self._h_vel_out = h = torch.empty_like(self._h_vel)
+        h.copy_(self.vel)
+        return h.numpy()[: self.n_i]
+
     def positions_host(self) -> np.ndarray:
         """Current positions (N, 3): one D2H of the packed rows into pinned memory."""
         self._h_out.copy_(self.pos_cur)

@@ -143,6 +143,14 @@ def _matrix(sys_, field: str) -> np.ndarray:
     return np.asarray(data)
 
 
+def _columns(sys_, field: str):
+    """(x, y, z) 1-D views of positions or velocities (no copy), either layout."""
+    data = getattr(sys_, field)
+    if _value(sys_.layout) == "soa":
+        return tuple(data)
+    return data[:, 0], data[:, 1], data[:, 2]
+
+
 def _store(state, field: str, values: np.ndarray) -> None:
     """Write (N,3) results into a system's own buffers, preserving its layout."""
     data = getattr(state, field)
@@ -191,7 +199,8 @@ def compute_accelerations(sys_, params, variant: Optional[KernelVariant] = None,
     pos = _matrix(sys_, "positions")
     m = np.asarray(sys_.masses, dtype)
     eps2 = params.softening_sq
-    st = _resident_state(pos, np.zeros_like(pos), m, dtype)
+    z = np.zeros(pos.shape[0], dtype)
+    st = _resident_state((pos[:, 0], pos[:, 1], pos[:, 2]), (z, z, z), m, dtype)
     a = st.accelerations(params.gravitational_constant, eps2, kernel_flags(m, eps2, dtype))
     host = a[:, :3].cpu().numpy()
     out.x[...] = host[:, 0]
@@ -246,7 +255,7 @@ def simulate_arrays(positions, velocities, masses, softening_sq: float, dt: floa
     if _distributed_world(group) > 1:
         from .sharded import simulate_sharded
         return simulate_sharded(pos, vel, m, dtype, G, dt, softening_sq, steps, group=group)
-    st = _resident_state(pos, vel, m, dtype)
+    st = _resident_state((pos[:, 0], pos[:, 1], pos[:, 2]), (vel[:, 0], vel[:, 1], vel[:, 2]), m, dtype)
     st.simulate(G, dt, softening_sq, steps, kernel_flags(m, softening_sq, dtype))
     return st.positions_host(), st.velocities_host()
 
@@ -260,7 +269,7 @@ def _resident_state(pos, vel, m, dtype):
     import torch
 
     from .device import DeviceState
-    key = (pos.shape[0], np.dtype(dtype).str, torch.cuda.current_device())
+    key = (m.shape[0], np.dtype(dtype).str, torch.cuda.current_device())
     st = _STATE_CACHE.get(key)
     if st is None:
         if len(_STATE_CACHE) >= 4:
@@ -276,14 +285,32 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
     system (same class, layout and precision); ``sys_`` is not modified."""
     if variant is not None:
         _check(sys_, variant, None)
-    state = sys_.copy()
-    pos, vel = simulate_arrays(_matrix(sys_, "positions"), _matrix(sys_, "velocities"), sys_.masses,
-                               params.softening_sq, params.dt, params.steps,
-                               params.gravitational_constant, precision=_value(sys_.precision),
-                               group=group)
-    _store(state, "positions", pos)
-    _store(state, "velocities", vel)
-    return state
+    if params.steps < 1:
+        raise ValueError("steps must be >= 1")
+    n, dtype = _count(sys_), _dtype(sys_)
+    if _distributed_world(group) > 1 or n < 1:
+        state = sys_.copy()
+        pos, vel = simulate_arrays(_matrix(sys_, "positions"), _matrix(sys_, "velocities"), sys_.masses,
+                                   params.softening_sq, params.dt, params.steps,
+                                   params.gravitational_constant, precision=_value(sys_.precision),
+                                   group=group)
+        _store(state, "positions", pos)
+        _store(state, "velocities", vel)
+        return state
+    # Single GPU: columns go straight into the pinned staging of the resident
+    # state and the result arrays are cut straight from the pinned readback.
+    from .device import kernel_flags
+    m = np.asarray(sys_.masses, dtype)
+    st = _resident_state(_columns(sys_, "positions"), _columns(sys_, "velocities"), m, dtype)
+    st.simulate(params.gravitational_constant, params.dt, params.softening_sq, params.steps,
+                kernel_flags(m, params.softening_sq, dtype))
+    hp = st.positions_packed()
+    pos = tuple(np.ascontiguousarray(hp[:, k]) for k in range(3))
+    hv = st.velocities_packed()
+    vel = tuple(np.ascontiguousarray(hv[:, k]) for k in range(3))
+    if _value(sys_.layout) != "soa":
+        pos, vel = np.ascontiguousarray(hp[:, :3]), np.ascontiguousarray(hv[:, :3])
+    return type(sys_)(sys_.layout, sys_.precision, pos, vel, sys_.masses.copy())
 
 
 def diagnostics_gpu(sys_, params) -> dict:
