@@ -50,6 +50,15 @@
 #ifndef NB_F32_PIPE
 #define NB_F32_PIPE 0
 #endif
+#ifndef NB_F32_PACKED
+#define NB_F32_PACKED 1
+#endif
+#ifndef NB_F32_MATH
+#define NB_F32_MATH 0
+#endif
+#ifndef NB_F32_STAGEWISE
+#define NB_F32_STAGEWISE 0
+#endif
 #ifndef NB_F32_RCP_PAIRS
 #define NB_F32_RCP_PAIRS 0
 #endif
@@ -110,6 +119,7 @@ __device__ __forceinline__ f2x pk(float lo, float hi) {
 __device__ __forceinline__ void upk(f2x v, float& lo, float& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
+#if NB_F32_PACKED
 __device__ __forceinline__ f2x add2(f2x a, f2x b) {
   f2x d;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -124,6 +134,37 @@ __device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
   f2x d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
+}
+#else  // ladder rung without packed FP32x2: the same arithmetic as scalar FADD/FMUL/FFMA
+__device__ __forceinline__ f2x add2(f2x a, f2x b) {
+  float al, ah, bl, bh;
+  upk(a, al, ah);
+  upk(b, bl, bh);
+  return pk(__fadd_rn(al, bl), __fadd_rn(ah, bh));
+}
+__device__ __forceinline__ f2x mul2(f2x a, f2x b) {
+  float al, ah, bl, bh;
+  upk(a, al, ah);
+  upk(b, bl, bh);
+  return pk(__fmul_rn(al, bl), __fmul_rn(ah, bh));
+}
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
+  float al, ah, bl, bh, cl, ch;
+  upk(a, al, ah);
+  upk(b, bl, bh);
+  upk(c, cl, ch);
+  return pk(__fmaf_rn(al, bl, cl), __fmaf_rn(ah, bh, ch));
+}
+#endif
+
+// m * d2^(-3/2) for one lane in the reference's algebraic forms (ladder rungs):
+// NB_F32_MATH 1 = recip (_accel_cy.pyx:86-94), 2 = pow (_accel_cy.pyx:42-49).
+__device__ __forceinline__ float w_reference_form(float d2, float m) {
+#if NB_F32_MATH == 2
+  return __fdiv_rn(m, powf(d2, 1.5f));
+#else
+  return __fmul_rn(m, __frcp_rn(__fmul_rn(d2, __fsqrt_rn(d2))));
+#endif
 }
 
 // ---------------------------------------------------------------- FP32 core
@@ -172,8 +213,49 @@ struct CoreF32 {
   // order): consecutive instructions share the broadcast source operand, and the
   // accumulate -- the instruction with three distinct register pairs, which the
   // register file cannot feed at full rate -- gets the most reuse.
+  __device__ __forceinline__ f2x weight(f2x d2, f2x mj, int jj, int q) const {
+    float d2a, d2b;
+    upk(d2, d2a, d2b);
+    f2x w;
+#if NB_F32_MATH == 0
+    const f2x r = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
+    // The first NB_F32_RCP_PAIRS pairs take r^2 from MUFU.RCP instead of an
+    // FMUL2 (an experiment: moving work to the XU pipe; off by default).
+    const f2x r2 = q < NB_F32_RCP_PAIRS ? pk(rcp_mufu(d2a), rcp_mufu(d2b)) : mul2(r, r);
+    // UNI (all masses equal): m is applied once to the finished sum, saving
+    // one FMUL2 of 12 per interaction pair.
+    w = UNI ? mul2(r2, r) : mul2(mul2(r, mj), r2);
+#else
+    float ma, mb;
+    upk(mj, ma, mb);
+    w = pk(w_reference_form(d2a, UNI ? 1.f : ma), w_reference_form(d2b, UNI ? 1.f : mb));
+#endif
+    if (MASK) {
+      float wa, wb;
+      upk(w, wa, wb);
+      if (jj == selfj[2 * q]) wa = 0.f;
+      if (jj == selfj[2 * q + 1]) wb = 0.f;
+      w = pk(wa, wb);
+    }
+    return w;
+  }
+
   __device__ __forceinline__ void interact(const F4& pj, int jj) {
     const f2x xj = pk(pj.x, pj.x), yj = pk(pj.y, pj.y), zj = pk(pj.z, pj.z), mj = pk(pj.w, pj.w);
+#if !NB_F32_STAGEWISE
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {  // ladder rung: per-pair order
+      const f2x dx = add2(xj, nx[q]), dy = add2(yj, ny[q]), dz = add2(zj, nz[q]);
+      f2x d2 = fma2(dx, dx, e2);
+      d2 = fma2(dy, dy, d2);
+      d2 = fma2(dz, dz, d2);
+      const f2x w = weight(d2, mj, jj, q);
+      tx[q] = fma2(dx, w, tx[q]);
+      ty[q] = fma2(dy, w, ty[q]);
+      tz[q] = fma2(dz, w, tz[q]);
+    }
+    return;
+#endif
     f2x dx[KP], dy[KP], dz[KP], d2[KP], w[KP];
 #pragma unroll
     for (int q = 0; q < KP; ++q) dx[q] = add2(xj, nx[q]);
@@ -188,24 +270,7 @@ struct CoreF32 {
 #pragma unroll
     for (int q = 0; q < KP; ++q) d2[q] = fma2(dz[q], dz[q], d2[q]);
 #pragma unroll
-    for (int q = 0; q < KP; ++q) {
-      float d2a, d2b;
-      upk(d2[q], d2a, d2b);
-      const f2x r = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
-      // The first NB_F32_RCP_PAIRS pairs take r^2 from MUFU.RCP instead of an
-      // FMUL2, moving work from the saturated FMA pipe to the half-idle XU pipe.
-      const f2x r2 = q < NB_F32_RCP_PAIRS ? pk(rcp_mufu(d2a), rcp_mufu(d2b)) : mul2(r, r);
-      // UNI (all masses equal): m is applied once to the finished sum, saving
-      // one FMUL2 of 12 per interaction pair.
-      w[q] = UNI ? mul2(r2, r) : mul2(mul2(r, mj), r2);
-      if (MASK) {
-        float wa, wb;
-        upk(w[q], wa, wb);
-        if (jj == selfj[2 * q]) wa = 0.f;
-        if (jj == selfj[2 * q + 1]) wb = 0.f;
-        w[q] = pk(wa, wb);
-      }
-    }
+    for (int q = 0; q < KP; ++q) w[q] = weight(d2[q], mj, jj, q);
 #pragma unroll
     for (int q = 0; q < KP; ++q) {
       tx[q] = fma2(w[q], dx[q], tx[q]);

@@ -14,10 +14,26 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "rcp1": {"NB_F32_RCP_PAIRS": 1},
-    "rcp2": {"NB_F32_RCP_PAIRS": 2},
-    "rcp3": {"NB_F32_RCP_PAIRS": 3},
 }
+
+# GPU optimisation ladder: the reference's ladder axes --
+# math form (pow / recip), blocking, SIMD-friendly layout, precision -- mapped
+# onto GPU knobs, each rung adding one change to the previous one (FP32, C3).
+LADDER = [
+    ("L0 pow form, scalar FP32, K=2, no unroll, per-pair order",
+     {"NB_F32_MATH": 2, "NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_UNROLL": 1, "NB_F32_STAGEWISE": 0}),
+    ("L1 + recip form (reference's fastest CPU rung)",
+     {"NB_F32_MATH": 1, "NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_UNROLL": 1, "NB_F32_STAGEWISE": 0}),
+    ("L2 + MUFU rsqrt form",
+     {"NB_F32_MATH": 0, "NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_UNROLL": 1, "NB_F32_STAGEWISE": 0}),
+    ("L3 + unrolled source loop (x16)",
+     {"NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_STAGEWISE": 0}),
+    ("L4 + register blocking, 6 targets/thread",
+     {"NB_F32_PACKED": 0, "NB_F32_STAGEWISE": 0}),
+    ("L5 + packed FFMA2/FADD2/FMUL2 (shipped)", {}),
+    ("L5' (alternative) stage-wise source order across the pairs", {"NB_F32_STAGEWISE": 1}),
+]
+VARIANTS.update({f"ladder{i}": d for i, (_, d) in enumerate(LADDER)})
 
 
 def build_one(name, defs):
@@ -125,8 +141,30 @@ def run(configs):
         json.dump(results, f, indent=1)
 
 
+def ladder_report(path):
+    res = json.load(open(os.path.join(REPO, "gpurun_out", "variants.json")))
+    lines = ["# GPU optimisation ladder (FP32, C3: N=131072, 10 steps, 1 B200)", "",
+             "Each rung adds one change to the previous rung; rates from `tools/variants.py run`",
+             "(`nb_dev_simulate`, best of 3). Fraction = 20 flop/interaction / nominal FP32 peak.", "",
+             "| rung | interactions/s | frac of nominal FP32 | speed-up vs L0 | vs previous |",
+             "|---|---|---|---|---|"]
+    base = prev = None
+    for i, (name, _) in enumerate(LADDER):
+        r = res.get(f"C3-f32/ladder{i}")
+        if r is None:
+            continue
+        base = base or r["rate"]
+        lines.append(f"| {name} | {r['rate']:.3e} | {r['frac']:.3f} | {r['rate'] / base:.2f}x | "
+                     f"{(r['rate'] / prev if prev else 1.0):.2f}x |")
+        prev = r["rate"]
+    open(path, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "build":
         build()
+    elif sys.argv[1] == "ladder-report":
+        ladder_report(sys.argv[2])
     else:
         run(sys.argv[2:] or ["C3-f32", "C2", "C3-f64"])
