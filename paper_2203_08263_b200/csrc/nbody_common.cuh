@@ -63,12 +63,6 @@ __device__ __forceinline__ float rsqrt_mufu(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// Bare MUFU.RCP (FTZ, <= 1 ulp).
-__device__ __forceinline__ float rcp_mufu(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 // Bare MUFU.RSQ64H seed (about 2^-22 relative); refined by the caller.
 __device__ __forceinline__ double rsqrt_seed(double x) {
   double y;

@@ -47,9 +47,6 @@
 #ifndef NB_F32_UNROLL
 #define NB_F32_UNROLL 16
 #endif
-#ifndef NB_F32_PIPE
-#define NB_F32_PIPE 0
-#endif
 #ifndef NB_F32_PACKED
 #define NB_F32_PACKED 1
 #endif
@@ -58,9 +55,6 @@
 #endif
 #ifndef NB_F32_STAGEWISE
 #define NB_F32_STAGEWISE 0
-#endif
-#ifndef NB_F32_RCP_PAIRS
-#define NB_F32_RCP_PAIRS 0
 #endif
 #ifndef NB_CHUNK
 #define NB_CHUNK 16
@@ -219,9 +213,9 @@ struct CoreF32 {
     f2x w;
 #if NB_F32_MATH == 0
     const f2x r = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
-    // The first NB_F32_RCP_PAIRS pairs take r^2 from MUFU.RCP instead of an
-    // FMUL2 (an experiment: moving work to the XU pipe; off by default).
-    const f2x r2 = q < NB_F32_RCP_PAIRS ? pk(rcp_mufu(d2a), rcp_mufu(d2b)) : mul2(r, r);
+    // r^2 by FMUL2.  (Taking it from MUFU.RCP for some pairs, to shift work to
+    // the XU pipe, was measured slower: the XU pipe saturates first.)
+    const f2x r2 = mul2(r, r);
     // UNI (all masses equal): m is applied once to the finished sum, saving
     // one FMUL2 of 12 per interaction pair.
     w = UNI ? mul2(r2, r) : mul2(mul2(r, mj), r2);
@@ -278,67 +272,13 @@ struct CoreF32 {
       tz[q] = fma2(w[q], dz[q], tz[q]);
     }
   }
-  // Stage A of a source body: separations, d2 and the MUFU.RSQ pair.
-  __device__ __forceinline__ void stage_a(const F4& pj, f2x* dx, f2x* dy, f2x* dz, f2x* r) const {
-    const f2x xj = pk(pj.x, pj.x), yj = pk(pj.y, pj.y), zj = pk(pj.z, pj.z);
-#pragma unroll
-    for (int q = 0; q < KP; ++q) {
-      dx[q] = add2(xj, nx[q]);
-      dy[q] = add2(yj, ny[q]);
-      dz[q] = add2(zj, nz[q]);
-      f2x d2 = fma2(dx[q], dx[q], e2);
-      d2 = fma2(dy[q], dy[q], d2);
-      d2 = fma2(dz[q], dz[q], d2);
-      float d2a, d2b;
-      upk(d2, d2a, d2b);
-      r[q] = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
-    }
-  }
-  // Stage B: w = m r^3 and the accumulation.
-  __device__ __forceinline__ void stage_b(float m, int jj, const f2x* dx, const f2x* dy, const f2x* dz,
-                                          const f2x* r) {
-    const f2x mj = pk(m, m);
-#pragma unroll
-    for (int q = 0; q < KP; ++q) {
-      const f2x r2 = mul2(r[q], r[q]);
-      f2x w = UNI ? mul2(r2, r[q]) : mul2(mul2(r[q], mj), r2);
-      if (MASK) {
-        float wa, wb;
-        upk(w, wa, wb);
-        if (jj == selfj[2 * q]) wa = 0.f;
-        if (jj == selfj[2 * q + 1]) wb = 0.f;
-        w = pk(wa, wb);
-      }
-      tx[q] = fma2(dx[q], w, tx[q]);
-      ty[q] = fma2(dy[q], w, ty[q]);
-      tz[q] = fma2(dz[q], w, tz[q]);
-    }
-  }
-  // A full tile, software-pipelined by one source body: stage A of body j+1
-  // (whose MUFUs have a whole stage of independent FP32 work to hide behind)
-  // is interleaved with stage B of body j.
+  // A full tile of TJ source bodies, unrolled UNROLL_ deep.  (Software-
+  // pipelining stage A of body j+1 against stage B of body j was measured
+  // slower: profiles/variants_r01_sweep2.txt, "pipe".)
   template <int TJ>
   __device__ __forceinline__ void full_tile(const F4* tb) {
-#if NB_F32_PIPE
-    f2x dx[KP], dy[KP], dz[KP], r[KP];
-    F4 p = tb[0];
-    stage_a(p, dx, dy, dz, r);
-    float m = p.w;
-#pragma unroll UNROLL_
-    for (int jj = 1; jj < TJ; ++jj) {
-      const F4 q = tb[jj];
-      f2x dx1[KP], dy1[KP], dz1[KP], r1[KP];
-      stage_a(q, dx1, dy1, dz1, r1);
-      stage_b(m, jj - 1, dx, dy, dz, r);
-#pragma unroll
-      for (int k = 0; k < KP; ++k) { dx[k] = dx1[k]; dy[k] = dy1[k]; dz[k] = dz1[k]; r[k] = r1[k]; }
-      m = q.w;
-    }
-    stage_b(m, TJ - 1, dx, dy, dz, r);
-#else
 #pragma unroll UNROLL_
     for (int jj = 0; jj < TJ; ++jj) interact(tb[jj], jj);
-#endif
   }
   __device__ __forceinline__ void end_tile() {
 #pragma unroll
