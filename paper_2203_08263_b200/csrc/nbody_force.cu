@@ -53,6 +53,9 @@
 #ifndef NB_F32_MATH
 #define NB_F32_MATH 0
 #endif
+#ifndef NB_F32_SUMS_IN_REGS
+#define NB_F32_SUMS_IN_REGS 0
+#endif
 #ifndef NB_F32_STAGEWISE
 #define NB_F32_STAGEWISE 0
 #endif
@@ -170,7 +173,12 @@ struct CoreF32 {
   using R = float;
   static constexpr int K = K_;
   static constexpr int KP = K / 2;
+#if NB_F32_SUMS_IN_REGS
+  static constexpr int SMEM_SUMS = 1;
+  double rs[3 * K];  // FP64 segment sums in registers (1 CTA/SM leaves room)
+#else
   static constexpr int SMEM_SUMS = 3 * K;  // doubles per thread
+#endif
   f2x nx[KP], ny[KP], nz[KP];  // negated target positions, paired
   f2x tx[KP], ty[KP], tz[KP];  // FP32 partial sums of the current tile
   int selfj[K];
@@ -191,11 +199,18 @@ struct CoreF32 {
     ny[q] = add2(0ull, pk(-p0.y, -p1.y));
     nz[q] = add2(0ull, pk(-p0.z, -p1.z));
   }
-  __device__ __forceinline__ double sum(int d, int k) const { return ss[(d * K + k) * stride]; }
-  __device__ __forceinline__ void set_sum(int d, int k, double v) { ss[(d * K + k) * stride] = v; }
+#if NB_F32_SUMS_IN_REGS
+  __device__ __forceinline__ double& acc_ref(int i) { return rs[i]; }
+  __device__ __forceinline__ double acc_val(int i) const { return rs[i]; }
+#else
+  __device__ __forceinline__ double& acc_ref(int i) { return ss[i * stride]; }
+  __device__ __forceinline__ double acc_val(int i) const { return ss[i * stride]; }
+#endif
+  __device__ __forceinline__ double sum(int d, int k) const { return acc_val(d * K + k); }
+  __device__ __forceinline__ void set_sum(int d, int k, double v) { acc_ref(d * K + k) = v; }
   __device__ __forceinline__ void zero_sums() {
 #pragma unroll
-    for (int i = 0; i < 3 * K; ++i) ss[i * stride] = 0.0;
+    for (int i = 0; i < 3 * K; ++i) acc_ref(i) = 0.0;
   }
   __device__ __forceinline__ void begin_tile() {
 #pragma unroll
@@ -285,14 +300,14 @@ struct CoreF32 {
     for (int q = 0; q < KP; ++q) {
       float a, b;
       upk(tx[q], a, b);
-      ss[(0 * K + 2 * q) * stride] += (double)a;
-      ss[(0 * K + 2 * q + 1) * stride] += (double)b;
+      acc_ref(0 * K + 2 * q) += (double)a;
+      acc_ref(0 * K + 2 * q + 1) += (double)b;
       upk(ty[q], a, b);
-      ss[(1 * K + 2 * q) * stride] += (double)a;
-      ss[(1 * K + 2 * q + 1) * stride] += (double)b;
+      acc_ref(1 * K + 2 * q) += (double)a;
+      acc_ref(1 * K + 2 * q + 1) += (double)b;
       upk(tz[q], a, b);
-      ss[(2 * K + 2 * q) * stride] += (double)a;
-      ss[(2 * K + 2 * q + 1) * stride] += (double)b;
+      acc_ref(2 * K + 2 * q) += (double)a;
+      acc_ref(2 * K + 2 * q + 1) += (double)b;
     }
   }
 };

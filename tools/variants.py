@@ -14,6 +14,10 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
+    "regs": {"NB_F32_SUMS_IN_REGS": 1},
+    "regs_k8": {"NB_F32_SUMS_IN_REGS": 1, "NB_F32_K": 8},
+    "regs_k4": {"NB_F32_SUMS_IN_REGS": 1, "NB_F32_K": 4},
+    "regs_k8_t128": {"NB_F32_SUMS_IN_REGS": 1, "NB_F32_K": 8, "NB_F32_T": 128, "NB_F32_MINB": 2},
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
@@ -33,7 +37,7 @@ LADDER = [
     ("L5 + packed FFMA2/FADD2/FMUL2 (shipped)", {}),
     ("L5' (alternative) stage-wise source order across the pairs", {"NB_F32_STAGEWISE": 1}),
 ]
-VARIANTS.update({f"ladder{i}": d for i, (_, d) in enumerate(LADDER)})
+# VARIANTS.update({f"ladder{i}": d for i, (_, d) in enumerate(LADDER)})  # enable for the ladder run
 
 
 def build_one(name, defs):
