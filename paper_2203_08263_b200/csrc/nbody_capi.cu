@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -39,6 +40,17 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
 
+// Bodies up to which nb_dev_simulate runs the whole loop in one persistent
+// cooperative launch (NB_PERSISTENT_MAX_N overrides; 0 disables).
+int64_t persistent_max_n() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* env = getenv("NB_PERSISTENT_MAX_N");
+    v = env ? atoll(env) : 65536;
+  }
+  return v;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // Make the device that owns `p` current for this runtime instance.  The library
@@ -55,11 +67,11 @@ cudaError_t bind_device_of(const void* p) {
 }
 
 template <typename R>
-int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
+int make_step_args(StepArgs<R>& a, const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
              int64_t j_count, double g, double eps2, double dt, int mode, int flags,
              double* carry, int carry_mode, void* acc4, void* vel4, void* pos4_next,
              void* workspace, int64_t workspace_bytes, void* stream,
-             void* const* peers = nullptr, int n_peers = 0) {
+             void* const* peers, int n_peers) {
   if (n_all < 1 || i_begin < 0 || n_i < 0 || i_begin + n_i > n_all)
     return fail(NB_ERR_ARG, "target range [i_begin, i_begin+n_i) must lie in [0, n_all)");
   if (j_begin < 0 || j_begin >= n_all || j_count < 0 || j_count > n_all)
@@ -74,7 +86,7 @@ int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int6
   for (int q = 0; q < n_peers; ++q)
     if (!peers[q] || !aligned16(peers[q]) || peers[q] == pos4)
       return fail(NB_ERR_ARG, "peer next-position buffers must be 16-byte aligned and must not alias pos4");
-  if (n_i == 0) return NB_OK;
+  if (n_i == 0) return -1;  // nothing to launch
   if (!pos4 || !aligned16(pos4)) return fail(NB_ERR_ARG, "pos4 must be a 16-byte aligned device pointer");
   const bool finalize = carry_mode != 1;
   if (finalize && (!acc4 || !aligned16(acc4))) return fail(NB_ERR_ARG, "acc4 must be a 16-byte aligned device pointer");
@@ -90,7 +102,7 @@ int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int6
     return fail(NB_ERR_WORKSPACE, "workspace smaller than nb_dev_workspace_bytes(): need " + std::to_string(need));
 
   const StepGeometry geo = step_geometry<R>(n_i, j_count);
-  StepArgs<R> a{};
+  a = StepArgs<R>{};
   a.pos = static_cast<const V4<R>*>(pos4);
   a.n_all = n_all; a.i_begin = i_begin; a.n_i = n_i; a.j_begin = j_begin; a.j_count = j_count;
   a.eps2 = (R)eps2;
@@ -103,6 +115,21 @@ int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int6
   a.slots = reinterpret_cast<double*>(static_cast<char*>(workspace) + counters_bytes(geo.n_iblocks));
   a.n_peers = n_peers;
   for (int q = 0; q < n_peers; ++q) a.peers[q] = static_cast<V4<R>*>(peers[q]);
+  (void)stream;
+  return NB_OK;
+}
+
+template <typename R>
+int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
+             int64_t j_count, double g, double eps2, double dt, int mode, int flags,
+             double* carry, int carry_mode, void* acc4, void* vel4, void* pos4_next,
+             void* workspace, int64_t workspace_bytes, void* stream,
+             void* const* peers = nullptr, int n_peers = 0) {
+  StepArgs<R> a;
+  int rc = make_step_args<R>(a, pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, flags, carry,
+                             carry_mode, acc4, vel4, pos4_next, workspace, workspace_bytes, stream, peers, n_peers);
+  if (rc == -1) return NB_OK;
+  if (rc) return rc;
   cudaError_t e = launch_step<R>(a, flags & (NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS),
                                  static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "launch_step");
@@ -118,6 +145,23 @@ int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, do
   if (steps < 1) return fail(NB_ERR_ARG, "steps must be >= 1");
   if (!(dt > 0.0)) return fail(NB_ERR_ARG, "dt must be positive");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!events && n <= persistent_max_n()) {
+    // small N: the whole loop in one cooperative launch (launch-bound otherwise)
+    StepArgs<R> a;
+    int rc = make_step_args<R>(a, pos_a, n, 0, n, 0, n, g, eps2, dt, NB_STEP_FIRST, flags, nullptr, 0, acc4, vel4,
+                               pos_b, ws, ws_bytes, stream, nullptr, 0);
+    if (rc && rc != -1) return rc;
+    if (rc == 0) {
+      cudaError_t e = launch_simulate_persistent<R>(a, flags & (NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS),
+                                                    static_cast<V4<R>*>(pos_a), static_cast<V4<R>*>(pos_b), steps, st);
+      if (e == cudaSuccess) {
+        if (final_in_b) *final_in_b = (steps & 1) ? 1 : 0;
+        return NB_OK;
+      }
+      if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported) return cuda_fail(e, "simulate_kernel");
+      cudaGetLastError();  // fall through to per-step launches
+    }
+  }
   void* cur = pos_a;
   void* nxt = pos_b;
   for (int64_t s = 0; s < steps; ++s) {

@@ -29,6 +29,7 @@
 #include "nbody_common.cuh"
 #include "nbody_kernels.h"
 
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 // Tuning knobs (overridable with -D for variant sweeps, tools/variants.py).
@@ -263,8 +264,7 @@ struct CoreF32 {
       ty[q] = fma2(dy, w, ty[q]);
       tz[q] = fma2(dz, w, tz[q]);
     }
-    return;
-#endif
+#else
     f2x dx[KP], dy[KP], dz[KP], d2[KP], w[KP];
 #pragma unroll
     for (int q = 0; q < KP; ++q) dx[q] = add2(xj, nx[q]);
@@ -286,6 +286,7 @@ struct CoreF32 {
       ty[q] = fma2(w[q], dy[q], ty[q]);
       tz[q] = fma2(w[q], dz[q], tz[q]);
     }
+#endif
   }
   // A full tile of TJ source bodies, unrolled UNROLL_ deep.  (Software-
   // pipelining stage A of body j+1 against stage B of body j was measured
@@ -431,7 +432,7 @@ __device__ __forceinline__ void finalize_body(const StepArgs<R>& a, int64_t il, 
     }
     if (a.mode != NB_STEP_MODE_FINAL) {  // kick-drift, _accel_cy.pyx:218-226
       const int64_t ig = a.i_begin + il;
-      V4<R> p = a.pos[ig];
+      V4<R> p = ld4_cg(a.pos + ig);
       const R dvx = mul_rn(ax, a.dt), dvy = mul_rn(ay, a.dt), dvz = mul_rn(az, a.dt);
       p.x = add_rn(p.x, mul_rn(add_rn(v.x, mul_rn(a.half, dvx)), a.dt));
       p.y = add_rn(p.y, mul_rn(add_rn(v.y, mul_rn(a.half, dvy)), a.dt));
@@ -449,8 +450,20 @@ __device__ __forceinline__ void finalize_body(const StepArgs<R>& a, int64_t il, 
 }
 
 // ---------------------------------------------------------------- stream-K kernel
-template <class Core, int T, int TJ, int MINB, int CH>
-__global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename Core::R> a) {
+// Coherent (L2) or read-only-path load of a source/target body: inside the
+// persistent multi-step kernel positions change between steps of ONE launch, so
+// they must not come through the non-coherent read-only path.
+template <bool COH, typename B>
+__device__ __forceinline__ B ldp(const B* p) {
+  if constexpr (COH) return ld4_cg(p);
+  else return ld4(p);
+}
+
+// One force(+update) pass of the stream-K decomposition: the body of
+// step_kernel, shared with the persistent multi-step simulate_kernel.
+template <class Core, int T, int TJ, int CH, bool COH>
+__device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
+                                          V4<typename Core::R> (*tile)[TJ], double* s_sums) {
   using R = typename Core::R;
   using B = V4<R>;
   constexpr int K = Core::K;
@@ -459,13 +472,6 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
   static_assert(TJ % T == 0, "tile must be a multiple of the block");
   static_assert(TJ % CH == 0, "tile must be a multiple of the stream-K chunk");
 
-  __shared__ B tile[2][TJ];
-  __shared__ double s_sums[Core::SMEM_SUMS * T];
-
-  // Programmatic dependent launch: wait for the previous kernel in the stream
-  // (positions it wrote), then let the fixup kernel be scheduled as our CTAs drain.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x;
   const int64_t c = blockIdx.x;
   const Sched S{a.units, a.grid};
@@ -485,8 +491,8 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
 #pragma unroll
     for (int q = 0; q < K / 2; ++q) {
       const int64_t i0 = b * IB + (2 * q) * T + tid, i1 = i0 + T;
-      core.set_pair(q, ld4(a.pos + a.i_begin + (i0 < a.n_i ? i0 : a.n_i - 1)),
-                    ld4(a.pos + a.i_begin + (i1 < a.n_i ? i1 : a.n_i - 1)));
+      core.set_pair(q, ldp<COH>(a.pos + a.i_begin + (i0 < a.n_i ? i0 : a.n_i - 1)),
+                    ldp<COH>(a.pos + a.i_begin + (i1 < a.n_i ? i1 : a.n_i - 1)));
     }
     core.zero_sums();
 
@@ -499,7 +505,7 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
           int64_t jg = a.j_begin + off;
           if (jg >= a.n_all) jg -= a.n_all;
           NB_DCHECK(jg >= 0 && jg < a.n_all);
-          stage[r] = ld4(a.pos + jg);
+          stage[r] = ldp<COH>(a.pos + jg);
         } else {
           stage[r] = B{};
         }
@@ -577,6 +583,17 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
   if (a.n_peers) __threadfence_system();  // peer stores visible before the rank barrier
 }
 
+template <class Core, int T, int TJ, int MINB, int CH>
+__global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename Core::R> a) {
+  __shared__ V4<typename Core::R> tile[2][TJ];
+  __shared__ double s_sums[Core::SMEM_SUMS * T];
+  // Programmatic dependent launch: wait for the previous kernel in the stream
+  // (positions it wrote), then let the fixup kernel be scheduled as our CTAs drain.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  step_body<Core, T, TJ, CH, false>(a, tile, s_sums);
+}
+
 // ---------------------------------------------------------------- split i-block fixup
 template <typename R, int IB>
 __device__ __forceinline__ void fixup_body(const StepArgs<R>& a, int64_t il);
@@ -612,6 +629,38 @@ __device__ __forceinline__ void fixup_body(const StepArgs<R>& a, int64_t il) {
     tz += q[2 * IB];
   }
   finalize_body<R>(a, il, tx, ty, tz);
+}
+
+// ---------------------------------------------------------------- persistent multi-step kernel
+// Small N is launch-bound (C1: 1M interactions per evaluation, ~0.4 us of math
+// against several us of launch + fixup per step).  This kernel runs the whole
+// velocity-Verlet loop of kernels.simulate in ONE cooperative launch: every step
+// is the same stream-K pass as step_kernel, a grid-wide barrier, the split-i-block
+// fixup spread over all CTAs, and a second barrier before the next step reads
+// the new positions.  Same decomposition, same partial-sum order: results are
+// bitwise identical to the per-launch path (tested).
+template <class Core, int T, int TJ, int MINB, int CH>
+__global__ void __launch_bounds__(T, MINB) simulate_kernel(StepArgs<typename Core::R> a,
+                                                          V4<typename Core::R>* pos_a,
+                                                          V4<typename Core::R>* pos_b, int64_t steps,
+                                                          int any_split) {
+  using R = typename Core::R;
+  constexpr int IB = T * Core::K;
+  __shared__ V4<R> tile[2][TJ];
+  __shared__ double s_sums[Core::SMEM_SUMS * T];
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  for (int64_t s = 0; s <= steps; ++s) {
+    a.mode = s == 0 ? NB_STEP_MODE_FIRST : (s < steps ? NB_STEP_MODE_KICK_DRIFT : NB_STEP_MODE_FINAL);
+    a.pos = (s & 1) ? pos_b : pos_a;
+    a.pos_next = (s & 1) ? pos_a : pos_b;
+    step_body<Core, T, TJ, CH, true>(a, tile, s_sums);
+    if (any_split) {
+      grid.sync();  // every partial slot of this step is written
+      for (int64_t il = blockIdx.x * (int64_t)T + threadIdx.x; il < a.n_i; il += (int64_t)gridDim.x * T)
+        fixup_body<R, IB>(a, il);
+    }
+    grid.sync();  // all new positions/velocities visible; nobody still reads the old buffer
+  }
 }
 
 // ---------------------------------------------------------------- configurations
@@ -734,6 +783,43 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
 }
 
 template <typename R>
+cudaError_t launch_simulate_persistent(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b, int64_t steps,
+                                       cudaStream_t stream) {
+  const StepGeometry g = step_geometry<R>(a.n_i, a.j_count);
+  a.n_tiles = g.n_tiles;
+  a.n_iblocks = g.n_iblocks;
+  a.units = g.units;
+  int grid = max_grid<R>();
+  if ((int64_t)grid > g.units) grid = (int)g.units;
+  a.grid = grid;
+  const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
+  a.uniform_mass = uni ? 1 : 0;
+  int any_split = 0;
+  for (int64_t b = 0; b < g.n_iblocks && !any_split; ++b)
+    any_split = host_cta_of(b * g.n_tiles, grid, g.units) != host_cta_of(b * g.n_tiles + g.n_tiles - 1, grid, g.units);
+  using C = Cfg<R>;
+  void* args[] = {&a, &pos_a, &pos_b, &steps, &any_split};
+  const void* fn;
+  if (mask_self && uni)
+    fn = reinterpret_cast<const void*>(&simulate_kernel<typename C::template Core<true, true>, C::T, C::TJ, C::MINB, NB_CHUNK>);
+  else if (mask_self)
+    fn = reinterpret_cast<const void*>(&simulate_kernel<typename C::template Core<true, false>, C::T, C::TJ, C::MINB, NB_CHUNK>);
+  else if (uni)
+    fn = reinterpret_cast<const void*>(&simulate_kernel<typename C::template Core<false, true>, C::T, C::TJ, C::MINB, NB_CHUNK>);
+  else
+    fn = reinterpret_cast<const void*>(&simulate_kernel<typename C::template Core<false, false>, C::T, C::TJ, C::MINB, NB_CHUNK>);
+  // co-residency: the cooperative grid must fit the device at this occupancy
+  int dev = 0, per_sm = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, C::T, 0);
+  if (grid > per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(C::T), args, 0, stream);
+  count_launch();
+  return e;
+}
+
+template <typename R>
 int64_t step_workspace_bytes(int64_t n_i) {
   const StepGeometry g = step_geometry<R>(n_i, 1);
   const int64_t counters = counters_bytes(g.n_iblocks);
@@ -745,6 +831,10 @@ template StepGeometry step_geometry<float>(int64_t, int64_t);
 template StepGeometry step_geometry<double>(int64_t, int64_t);
 template cudaError_t launch_step<float>(StepArgs<float>, int, cudaStream_t);
 template cudaError_t launch_step<double>(StepArgs<double>, int, cudaStream_t);
+template cudaError_t launch_simulate_persistent<float>(StepArgs<float>, int, V4<float>*, V4<float>*, int64_t,
+                                                      cudaStream_t);
+template cudaError_t launch_simulate_persistent<double>(StepArgs<double>, int, V4<double>*, V4<double>*, int64_t,
+                                                       cudaStream_t);
 template int64_t step_workspace_bytes<float>(int64_t);
 template int64_t step_workspace_bytes<double>(int64_t);
 

@@ -48,6 +48,9 @@ template <typename R> StepGeometry step_geometry(int64_t n_i, int64_t j_count);
 // flags: bit 0 exclude the self pair explicitly, bit 1 uniform masses.
 template <typename R> cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t s);
 template <typename R> int64_t step_workspace_bytes(int64_t n_i);
+// Whole simulate loop (steps drift steps + the final kick) in one cooperative launch.
+template <typename R> cudaError_t launch_simulate_persistent(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b,
+                                                             int64_t steps, cudaStream_t s);
 // Byte offset of the slot area inside the workspace (a 256-byte-aligned header).
 inline int64_t counters_bytes(int64_t n_iblocks) { return ((n_iblocks * 4 + 255) / 256) * 256; }
 

@@ -279,17 +279,23 @@ def test_runs_are_bitwise_reproducible(prec):
     np.testing.assert_array_equal(a, b)
 
 
-def test_simulate_timed_matches_simulate():
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("n,eps2", [(1000, 1e-3), (5000, 1e-3), (3000, 0.0), (40000, 1e-3)])
+def test_persistent_simulate_matches_per_launch(prec, n, eps2):
+    """Small N runs the whole loop in one cooperative launch (simulate_kernel);
+    nb_dev_simulate_timed always launches per step.  Same decomposition and
+    partial-sum order: bitwise identical results."""
     from paper_2203_08263_b200.device import DeviceState, kernel_flags
-    s = cube(5000, 12, "single")
+    s = cube(n, 12, prec)
     dt_ = s.precision.dtype
     a = DeviceState(s.position_matrix().astype(dt_), np.stack(s.velocities, 1), s.masses, dt_)
     b = DeviceState(s.position_matrix().astype(dt_), np.stack(s.velocities, 1), s.masses, dt_)
-    f = kernel_flags(s.masses, 1e-3, dt_)
-    a.simulate(1.0, 1e-3, 1e-3, 5, f)
-    ms = b.simulate_timed(1.0, 1e-3, 1e-3, 5, f)
+    f = kernel_flags(s.masses, eps2, dt_)
+    a.simulate(1.0, 1e-3, eps2, 5, f)
+    ms = b.simulate_timed(1.0, 1e-3, eps2, 5, f)
     assert len(ms) == 6 and all(t > 0 for t in ms)
     np.testing.assert_array_equal(a.positions_host(), b.positions_host())
+    np.testing.assert_array_equal(a.velocities_host(), b.velocities_host())
 
 
 def test_native_kernels_launched():
