@@ -46,7 +46,7 @@ int64_t persistent_max_n() {
   static int64_t v = -1;
   if (v < 0) {
     const char* env = getenv("NB_PERSISTENT_MAX_N");
-    v = env ? atoll(env) : 65536;
+    v = env ? atoll(env) : 8192;
   }
   return v;
 }

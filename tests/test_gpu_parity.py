@@ -280,7 +280,7 @@ def test_runs_are_bitwise_reproducible(prec):
 
 
 @pytest.mark.parametrize("prec", ["double", "single"])
-@pytest.mark.parametrize("n,eps2", [(1000, 1e-3), (5000, 1e-3), (3000, 0.0), (40000, 1e-3)])
+@pytest.mark.parametrize("n,eps2", [(1000, 1e-3), (5000, 1e-3), (3000, 0.0), (8000, 1e-3)])
 def test_persistent_simulate_matches_per_launch(prec, n, eps2):
     """Small N runs the whole loop in one cooperative launch (simulate_kernel);
     nb_dev_simulate_timed always launches per step.  Same decomposition and
@@ -301,7 +301,7 @@ def test_persistent_simulate_matches_per_launch(prec, n, eps2):
 def test_native_kernels_launched():
     before = _native.launch_count()
     nb.simulate(cube(64, 1, "single"), nb.SimParams(1.0, 1e-3, 1e-3, 2))
-    assert _native.launch_count() - before >= 3
+    assert _native.launch_count() - before >= 1  # small N: one persistent launch
 
 
 # --------------------------------------------------------------------------- sizes & edges
