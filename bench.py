@@ -147,6 +147,37 @@ def cpu_reference_rate(cfg, sys0, budget_s: float = 20.0, fixed_n: int = 0):
     return float(n) * n / t, {"kind": kind, "cores": threads, "seconds": t, "n": n}
 
 
+def cpu_rate_isolated(cfg_name: str, fixed_n: int = 0):
+    """cpu_reference_rate in a child process, so that a host whose ISA differs
+    from the build host of oracle/_ref (-march=native) cannot take the GPU arm
+    down with it: the compiled reference first, then the C port; None if both fail."""
+    for kind in ("reference", "port"):
+        cmd = [sys.executable, os.path.abspath(__file__), "--cpu-child", cfg_name, str(fixed_n), kind]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        except subprocess.TimeoutExpired:
+            continue
+        if r.returncode == 0 and r.stdout.strip():
+            try:
+                rate, desc = json.loads(r.stdout.strip().splitlines()[-1])
+                return rate, desc
+            except ValueError:
+                pass
+        print(f"cpu baseline ({kind}) failed: rc={r.returncode} {r.stderr[-300:]}", file=sys.stderr)
+    return None
+
+
+def _cpu_child(cfg_name: str, fixed_n: int, kind: str) -> None:
+    import paper_2203_08263_b200 as nb
+    from oracle import oracle as O
+    cfg = nb.BASELINE_CONFIGS[cfg_name]
+    if kind == "port":
+        O._ref_mod = None
+        O.ref_available = lambda: False
+    rate, desc = cpu_reference_rate(cfg, cfg.system(), fixed_n=fixed_n)
+    print(json.dumps([rate, desc]))
+
+
 # --------------------------------------------------------------------------- GPU arm
 
 def _dist_env():
@@ -349,12 +380,17 @@ def run_ours(args) -> dict:
         "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
-        rate, desc = cpu_reference_rate(cfg, sys0)
-        result["cpu_baseline"] = {
-            "value": rate, "unit": UNIT, "cores": desc["cores"], "kind": desc["kind"],
-            "sample": f"one force evaluation (N^2 = {desc['n'] ** 2:.3e} interactions) of the "
-                      f"{cfg.name} initial state through the reference's compiled accel_soa "
-                      f"(soa-recip, {desc['cores']} threads), {desc['seconds']:.2f} s"}
+        got = cpu_rate_isolated(args.config)
+        if got is None:
+            result["cpu_baseline"] = {"value": None, "unit": UNIT, "unavailable": "CPU reference failed on this host"}
+        else:
+            rate, desc = got
+            what = "the reference's compiled accel_soa" if desc["kind"] == "reference" else "the oracle C port"
+            result["cpu_baseline"] = {
+                "value": rate, "unit": UNIT, "cores": desc["cores"], "kind": desc["kind"],
+                "sample": f"one force evaluation (N^2 = {desc['n'] ** 2:.3e} interactions) of the "
+                          f"{cfg.name} initial state through {what} "
+                          f"(soa-recip, {desc['cores']} threads), {desc['seconds']:.2f} s"}
     if world > 1:
         dist.destroy_process_group()
     return result if rank == 0 else None
@@ -370,8 +406,15 @@ def run_reference(args) -> dict:
         return None
     cfg = nb.BASELINE_CONFIGS[args.config]
     sys0 = cfg.system()
+    probe = cpu_rate_isolated(args.config)  # also proves the compiled kernel runs on this host
+    if probe is None:
+        return {"impl": "reference", "unavailable": "the reference's compiled CPU kernel and its C port "
+                                                    "both failed on this host"}
+    rate, desc = probe
+    if desc["kind"] != "reference":
+        from oracle import oracle as O
+        O.ref_available = lambda: False
     # size the per-step sample so the whole run stays within ~3 minutes
-    rate, desc = cpu_reference_rate(cfg, sys0)
     budget = 150.0
     per_step = desc["seconds"]
     n_s = cfg.n
@@ -415,7 +458,11 @@ def main(argv=None):
                     help="N>1 position exchange: NCCL all-gather (default) or the fused peer-store epilogue")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-child", nargs=3, metavar=("CONFIG", "N", "KIND"), help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
+    if args.cpu_child:
+        _cpu_child(args.cpu_child[0], int(args.cpu_child[1]), args.cpu_child[2])
+        return
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     res = run_reference(args) if args.impl == "reference" else run_ours(args)
