@@ -20,12 +20,14 @@
 //    N >= 131072, tile partials + FP64 outer sums are at ~1e-7).
 //  * FP64: MUFU.RSQ64H seed + one cubic correction that yields m*r^3 directly
 //    (16 DP ops + 1 MUFU per interaction, no slow-path branch).
-//  * Work distribution is stream-K over the (i-block x j-tile) space: a
-//    persistent grid of SMs x occupancy CTAs, each owning an equal contiguous
-//    range of units, so every SM gets the same work at every N.  An i-block split
-//    between CTAs is combined through FP64 partial slots; the last CTA to arrive
-//    sums them in fixed CTA order (bitwise reproducible run to run) and runs the
-//    epilogue.
+//  * Work distribution is stream-K over the (i-block x 16-body source chunk)
+//    space: a persistent grid of SMs x occupancy CTAs, each owning an equal
+//    contiguous range of units, so every SM gets the same work at every N.  An
+//    i-block split between CTAs is combined through FP64 partial slots by
+//    fixup_kernel (programmatic dependent launch) in fixed CTA order -- bitwise
+//    reproducible run to run -- which then runs the epilogue.
+//  * Small N: simulate_kernel runs the whole multi-step loop in one cooperative
+//    launch with grid barriers (same decomposition, bitwise-identical results).
 #include "nbody_common.cuh"
 #include "nbody_kernels.h"
 
@@ -85,8 +87,8 @@
 
 namespace nb {
 
-// NB_CHECK builds (tools/check_build.sh) trap on any out-of-range index: the
-// stand-in for compute-sanitizer, which this pool does not offer.
+// NB_CHECK builds (python -m paper_2203_08263_b200._build --check) trap on any
+// out-of-range index: the stand-in for compute-sanitizer, closed on this pool.
 #ifdef NB_CHECK
 #define NB_DCHECK(cond) do { if (!(cond)) __trap(); } while (0)
 #else
