@@ -62,6 +62,9 @@
 #ifndef NB_F32_STAGEWISE
 #define NB_F32_STAGEWISE 0
 #endif
+#ifndef NB_TMA_STAGING
+#define NB_TMA_STAGING 0
+#endif
 #ifndef NB_CHUNK
 #define NB_CHUNK 16
 #endif
@@ -461,11 +464,45 @@ __device__ __forceinline__ B ldp(const B* p) {
   else return ld4(p);
 }
 
+// ---------------------------------------------------------------- TMA (bulk-copy) staging
+// NB_TMA_STAGING: source tiles arrive in shared memory by cp.async.bulk (the 1-D
+// TMA path) on an mbarrier instead of LDG -> registers -> STS.  One elected
+// thread issues each tile (two copies when the circular source range wraps).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // One force(+update) pass of the stream-K decomposition: the body of
 // step_kernel, shared with the persistent multi-step simulate_kernel.
 template <class Core, int T, int TJ, int CH, bool COH>
 __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
-                                          V4<typename Core::R> (*tile)[TJ], double* s_sums) {
+                                          V4<typename Core::R> (*tile)[TJ], double* s_sums,
+                                          uint64_t* mbar) {
   using R = typename Core::R;
   using B = V4<R>;
   constexpr int K = Core::K;
@@ -482,6 +519,7 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
 
   Core core;
   core.init(a.eps2, s_sums + tid, T);
+  uint32_t phase[2] = {0u, 0u};  // mbarrier phase parity per tile buffer (TMA staging)
 
   for (int64_t u = u_begin; u < u_end;) {
     const int64_t b = u / NT;
@@ -498,6 +536,24 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
     }
     core.zero_sums();
 
+#if NB_TMA_STAGING
+    constexpr bool kTma = !COH;
+#else
+    constexpr bool kTma = false;
+#endif
+    // TMA staging: thread 0 arms the tile's mbarrier with its byte count and
+    // issues the bulk copies; everyone waits on the barrier's current phase.
+    auto issue_tile = [&](int buf, int64_t lo) {
+      if (tid == 0) {
+        const int64_t cnt = min((int64_t)TJ, s1 - lo);
+        int64_t jg = a.j_begin + lo;
+        if (jg >= a.n_all) jg -= a.n_all;
+        const int64_t n1 = min(cnt, a.n_all - jg);
+        mbar_expect_tx(mbar + buf, (uint32_t)(cnt * sizeof(B)));
+        bulk_g2s(tile[buf], a.pos + jg, (uint32_t)(n1 * sizeof(B)), mbar + buf);
+        if (cnt > n1) bulk_g2s(tile[buf] + n1, a.pos, (uint32_t)((cnt - n1) * sizeof(B)), mbar + buf);
+      }
+    };
     B stage[PER];
     auto load_tile = [&](int64_t lo) {
 #pragma unroll
@@ -518,14 +574,24 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
       for (int r = 0; r < PER; ++r) tile[buf][r * T + tid] = stage[r];
     };
 
-    load_tile(s0);
-    store_tile(0);
-    __syncthreads();
+    if (kTma) {
+      if (s0 < s1) issue_tile(0, s0);
+    } else {
+      load_tile(s0);
+      store_tile(0);
+      __syncthreads();
+    }
 
     int buf = 0;
     for (int64_t lo = s0; lo < s1; lo += TJ) {
       const bool more = lo + TJ < s1;
-      if (more) load_tile(lo + TJ);
+      if (kTma) {
+        if (more) issue_tile(buf ^ 1, lo + TJ);  // buf^1 was released by the last __syncthreads
+        mbar_wait(mbar + buf, phase[buf]);
+        phase[buf] ^= 1u;
+      } else if (more) {
+        load_tile(lo + TJ);
+      }
       const int count = (int)min((int64_t)TJ, s1 - lo);
       if (Core::MASK_SELF) {
         int64_t base = a.j_begin + lo;
@@ -554,7 +620,7 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
         for (; jj < count; ++jj) core.interact(tb[jj], jj);
       }
       core.end_tile();
-      if (more) store_tile(buf ^ 1);
+      if (!kTma && more) store_tile(buf ^ 1);
       buf ^= 1;
       __syncthreads();
     }
@@ -587,13 +653,22 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
 
 template <class Core, int T, int TJ, int MINB, int CH>
 __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename Core::R> a) {
-  __shared__ V4<typename Core::R> tile[2][TJ];
+  __shared__ alignas(128) V4<typename Core::R> tile[2][TJ];
   __shared__ double s_sums[Core::SMEM_SUMS * T];
+  __shared__ alignas(8) uint64_t mbar[2];
+#if NB_TMA_STAGING
+  if (threadIdx.x == 0) {
+    mbar_init(mbar, 1);
+    mbar_init(mbar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+#endif
   // Programmatic dependent launch: wait for the previous kernel in the stream
   // (positions it wrote), then let the fixup kernel be scheduled as our CTAs drain.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
-  step_body<Core, T, TJ, CH, false>(a, tile, s_sums);
+  step_body<Core, T, TJ, CH, false>(a, tile, s_sums, mbar);
 }
 
 // ---------------------------------------------------------------- split i-block fixup
@@ -649,14 +724,14 @@ __global__ void __launch_bounds__(T, MINB) simulate_kernel(StepArgs<typename Cor
                                                           int any_split) {
   using R = typename Core::R;
   constexpr int IB = T * Core::K;
-  __shared__ V4<R> tile[2][TJ];
+  __shared__ alignas(128) V4<R> tile[2][TJ];
   __shared__ double s_sums[Core::SMEM_SUMS * T];
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   for (int64_t s = 0; s <= steps; ++s) {
     a.mode = s == 0 ? NB_STEP_MODE_FIRST : (s < steps ? NB_STEP_MODE_KICK_DRIFT : NB_STEP_MODE_FINAL);
     a.pos = (s & 1) ? pos_b : pos_a;
     a.pos_next = (s & 1) ? pos_a : pos_b;
-    step_body<Core, T, TJ, CH, true>(a, tile, s_sums);
+    step_body<Core, T, TJ, CH, true>(a, tile, s_sums, nullptr);
     if (any_split) {
       grid.sync();  // every partial slot of this step is written
       for (int64_t il = blockIdx.x * (int64_t)T + threadIdx.x; il < a.n_i; il += (int64_t)gridDim.x * T)

@@ -14,10 +14,8 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "regs": {"NB_F32_SUMS_IN_REGS": 1},
-    "regs_k8": {"NB_F32_SUMS_IN_REGS": 1, "NB_F32_K": 8},
-    "regs_k4": {"NB_F32_SUMS_IN_REGS": 1, "NB_F32_K": 4},
-    "regs_k8_t128": {"NB_F32_SUMS_IN_REGS": 1, "NB_F32_K": 8, "NB_F32_T": 128, "NB_F32_MINB": 2},
+    "tma": {"NB_TMA_STAGING": 1},
+    "tma_f64": {"NB_TMA_STAGING": 1},
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
