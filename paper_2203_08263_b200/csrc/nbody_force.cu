@@ -62,8 +62,8 @@
 #ifndef NB_F32_STAGEWISE
 #define NB_F32_STAGEWISE 0
 #endif
-#ifndef NB_TMA_STAGING
-#define NB_TMA_STAGING 0
+#ifndef NB_TMA_MIN_N
+#define NB_TMA_MIN_N 65536  // FP32 launches with >= this many targets and sources use TMA staging
 #endif
 #ifndef NB_CHUNK
 #define NB_CHUNK 16
@@ -465,9 +465,10 @@ __device__ __forceinline__ B ldp(const B* p) {
 }
 
 // ---------------------------------------------------------------- TMA (bulk-copy) staging
-// NB_TMA_STAGING: source tiles arrive in shared memory by cp.async.bulk (the 1-D
-// TMA path) on an mbarrier instead of LDG -> registers -> STS.  One elected
-// thread issues each tile (two copies when the circular source range wraps).
+// With TMA staging (large FP32 launches, use_tma) source tiles arrive in shared
+// memory by cp.async.bulk (the 1-D TMA path) on an mbarrier per buffer instead
+// of LDG -> registers -> STS.  Thread 0 issues each tile (two copies when the
+// circular source range wraps); every thread waits on the buffer's phase.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -499,7 +500,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 // One force(+update) pass of the stream-K decomposition: the body of
 // step_kernel, shared with the persistent multi-step simulate_kernel.
-template <class Core, int T, int TJ, int CH, bool COH>
+template <class Core, int T, int TJ, int CH, bool COH, bool TMA>
 __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
                                           V4<typename Core::R> (*tile)[TJ], double* s_sums,
                                           uint64_t* mbar) {
@@ -536,11 +537,7 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
     }
     core.zero_sums();
 
-#if NB_TMA_STAGING
-    constexpr bool kTma = !COH;
-#else
-    constexpr bool kTma = false;
-#endif
+    constexpr bool kTma = TMA && !COH;
     // TMA staging: thread 0 arms the tile's mbarrier with its byte count and
     // issues the bulk copies; everyone waits on the barrier's current phase.
     auto issue_tile = [&](int buf, int64_t lo) {
@@ -651,24 +648,24 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
   if (a.n_peers) __threadfence_system();  // peer stores visible before the rank barrier
 }
 
-template <class Core, int T, int TJ, int MINB, int CH>
+template <class Core, int T, int TJ, int MINB, int CH, bool TMA>
 __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename Core::R> a) {
   __shared__ alignas(128) V4<typename Core::R> tile[2][TJ];
   __shared__ double s_sums[Core::SMEM_SUMS * T];
   __shared__ alignas(8) uint64_t mbar[2];
-#if NB_TMA_STAGING
-  if (threadIdx.x == 0) {
-    mbar_init(mbar, 1);
-    mbar_init(mbar + 1, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(mbar, 1);
+      mbar_init(mbar + 1, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
   }
-  __syncthreads();
-#endif
   // Programmatic dependent launch: wait for the previous kernel in the stream
   // (positions it wrote), then let the fixup kernel be scheduled as our CTAs drain.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
-  step_body<Core, T, TJ, CH, false>(a, tile, s_sums, mbar);
+  step_body<Core, T, TJ, CH, false, TMA>(a, tile, s_sums, mbar);
 }
 
 // ---------------------------------------------------------------- split i-block fixup
@@ -731,7 +728,7 @@ __global__ void __launch_bounds__(T, MINB) simulate_kernel(StepArgs<typename Cor
     a.mode = s == 0 ? NB_STEP_MODE_FIRST : (s < steps ? NB_STEP_MODE_KICK_DRIFT : NB_STEP_MODE_FINAL);
     a.pos = (s & 1) ? pos_b : pos_a;
     a.pos_next = (s & 1) ? pos_a : pos_b;
-    step_body<Core, T, TJ, CH, true>(a, tile, s_sums, nullptr);
+    step_body<Core, T, TJ, CH, true, false>(a, tile, s_sums, nullptr);
     if (any_split) {
       grid.sync();  // every partial slot of this step is written
       for (int64_t il = blockIdx.x * (int64_t)T + threadIdx.x; il < a.n_i; il += (int64_t)gridDim.x * T)
@@ -761,10 +758,36 @@ template <> struct Cfg<double> {
   template <bool M, bool U> using Core = CoreF64M<M, U>;
 };
 
-template <typename R, bool M, bool U>
+template <typename R, bool M, bool U, bool TMA>
 static const void* kernel_ptr() {
   using C = Cfg<R>;
-  return reinterpret_cast<const void*>(&step_kernel<typename C::template Core<M, U>, C::T, C::TJ, C::MINB, NB_CHUNK>);
+  return reinterpret_cast<const void*>(
+      &step_kernel<typename C::template Core<M, U>, C::T, C::TJ, C::MINB, NB_CHUNK, TMA>);
+}
+
+// The step kernel for (exclude-self, uniform-mass, TMA staging).
+template <typename R>
+static const void* step_fn(bool mask, bool uni, bool tma) {
+  if (tma) {
+    if (mask) return uni ? kernel_ptr<R, true, true, true>() : kernel_ptr<R, true, false, true>();
+    return uni ? kernel_ptr<R, false, true, true>() : kernel_ptr<R, false, false, true>();
+  }
+  if (mask) return uni ? kernel_ptr<R, true, true, false>() : kernel_ptr<R, true, false, false>();
+  return uni ? kernel_ptr<R, false, true, false>() : kernel_ptr<R, false, false, false>();
+}
+
+// TMA (bulk-copy) staging for large FP32 launches: measured +0.6 % at
+// N=131072, -3 % at N=16384 (profiles/variants_r01_tma.txt).  NB_TMA=0/1 forces it.
+template <typename R>
+static bool use_tma(int64_t n_i, int64_t j_count) {
+  if (sizeof(R) != 4) return false;
+  static int forced = -2;
+  if (forced == -2) {
+    const char* env = getenv("NB_TMA");
+    forced = env ? atoi(env) : -1;
+  }
+  if (forced >= 0) return forced != 0;
+  return n_i >= NB_TMA_MIN_N && j_count >= NB_TMA_MIN_N;
 }
 
 template <typename R>
@@ -780,29 +803,30 @@ StepGeometry step_geometry(int64_t n_i, int64_t j_count) {
   return g;
 }
 
+// Persistent grid: SMs x resident CTAs per SM of the step kernels of one staging
+// mode (the smallest occupancy over the four variants, so every variant's grid
+// is fully resident).
 template <typename R>
-int max_grid() {
-  static int cached[64] = {};
+int max_grid(bool tma = false) {
+  static int cached[64][2] = {};
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
-  if (cached[dev]) return cached[dev];
+  if (cached[dev][tma]) return cached[dev][tma];
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int best = 1;
-  const void* fns[4] = {kernel_ptr<R, false, false>(), kernel_ptr<R, true, false>(),
-                        kernel_ptr<R, false, true>(), kernel_ptr<R, true, true>()};
+  int per_sm_min = 1 << 20;
   for (int m = 0; m < 4; ++m) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[m], Cfg<R>::T, 0);
-    if (per_sm < 1) per_sm = 1;
-    best = best > sms * per_sm ? best : sms * per_sm;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fn<R>(m & 1, m & 2, tma), Cfg<R>::T, 0);
+    per_sm_min = per_sm < per_sm_min ? per_sm : per_sm_min;
   }
+  int best = sms * (per_sm_min < 1 ? 1 : per_sm_min);
   // Experiment hook: NB_GRID_OVERRIDE=<ctas> replaces the persistent grid size.
   if (const char* env = getenv("NB_GRID_OVERRIDE")) {
     const int v = atoi(env);
     if (v > 0) best = v;
   }
-  cached[dev] = best;
+  cached[dev][tma] = best;
   return best;
 }
 
@@ -817,7 +841,8 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   a.n_tiles = g.n_tiles;
   a.n_iblocks = g.n_iblocks;
   a.units = g.units;
-  int grid = max_grid<R>();
+  const bool tma = use_tma<R>(a.n_i, a.j_count);
+  int grid = max_grid<R>(tma);
   if ((int64_t)grid > g.units) grid = (int)g.units;
   a.grid = grid;
   using C = Cfg<R>;
@@ -835,15 +860,8 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   cfg.stream = stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e;
-  if (mask_self && uni)
-    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<true, true>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
-  else if (mask_self)
-    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<true, false>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
-  else if (uni)
-    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<false, true>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
-  else
-    e = cudaLaunchKernelEx(&cfg, step_kernel<typename C::template Core<false, false>, C::T, C::TJ, C::MINB, NB_CHUNK>, a);
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchKernelExC(&cfg, step_fn<R>(mask_self, uni, tma), args);
   count_launch();
   if (e != cudaSuccess) return e;
 
@@ -867,7 +885,7 @@ cudaError_t launch_simulate_persistent(StepArgs<R> a, int flags, V4<R>* pos_a, V
   a.n_tiles = g.n_tiles;
   a.n_iblocks = g.n_iblocks;
   a.units = g.units;
-  int grid = max_grid<R>();
+  int grid = max_grid<R>(false);
   if ((int64_t)grid > g.units) grid = (int)g.units;
   a.grid = grid;
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
@@ -901,7 +919,8 @@ template <typename R>
 int64_t step_workspace_bytes(int64_t n_i) {
   const StepGeometry g = step_geometry<R>(n_i, 1);
   const int64_t counters = counters_bytes(g.n_iblocks);
-  const int64_t slots = 2 * (int64_t)max_grid<R>() * 3 * g.i_block * 8;
+  const int64_t grid = max_grid<R>(false) > max_grid<R>(true) ? max_grid<R>(false) : max_grid<R>(true);
+  const int64_t slots = 2 * grid * 3 * g.i_block * 8;
   return counters + slots;
 }
 

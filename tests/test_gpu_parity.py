@@ -270,9 +270,10 @@ def test_momentum_conserved_from_rest():
     assert np.linalg.norm(m @ v) <= 1e-9 * float(np.sum(m * np.linalg.norm(v, axis=1)))
 
 
-@pytest.mark.parametrize("prec", ["double", "single"])
-def test_runs_are_bitwise_reproducible(prec):
-    s = cube(20000, 8, prec)
+@pytest.mark.parametrize("prec,n", [("double", 20000), ("single", 20000), ("single", 70000)])
+def test_runs_are_bitwise_reproducible(prec, n):
+    """Also covers the TMA-staged FP32 path (N >= 65536)."""
+    s = cube(n, 8, prec)
     p = nb.SimParams(1.0, 1e-3, 1e-3, 3)
     a = nb.simulate(s, p).position_matrix()
     b = nb.simulate(s, p).position_matrix()
@@ -355,6 +356,27 @@ def test_full_size_accelerations_row_sampled(cfg_name, oracle):
     dev = nb_accel_dev(a[rows], want)
     print(cfg_name, "accel_dev", dev)
     assert dev <= tol
+
+
+def test_tma_staged_path_with_wrapping_source_ranges(oracle):
+    """FP32 launches with >= 65536 targets and sources stage tiles by
+    cp.async.bulk; a circular source range that wraps past N (the multi-GPU
+    second phase) needs two bulk copies per tile.  Split the source range at an
+    odd offset (carry phases) and compare with the oracle."""
+    from paper_2203_08263_b200.device import DeviceState, kernel_flags
+    n = 70001
+    s = cube(n, 44, "single")
+    st = DeviceState(s.position_matrix().astype(np.float32), np.stack(s.velocities, 1), s.masses, np.float32)
+    f = kernel_flags(s.masses, 1e-3, np.float32)
+    out = __import__("torch").zeros((n, 4), dtype=__import__("torch").float32, device="cuda")
+    split = 12345  # phase 1: sources [12345, 12345+65537) mod n wraps; phase 2: the rest
+    st.step(1.0, 1e-3, 0.0, 0, f, j_begin=split, j_count=65537, carry_mode=1, acc_out=out)
+    st.step(1.0, 1e-3, 0.0, 0, f, j_begin=(split + 65537) % n, j_count=n - 65537, carry_mode=2, acc_out=out)
+    got = out[:, :3].cpu().numpy()
+    rows = np.arange(0, n, 701)
+    pos = s.position_matrix()
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)), s.masses, rows, 1.0, 1e-3)
+    assert nb_accel_dev(got[rows], want) <= F32_ACC_TOL
 
 
 def test_plummer_row_sampled(oracle):

@@ -15,7 +15,10 @@ OUT = os.path.join(HERE, "variants")
 VARIANTS = {
     "base": {},
     "tma": {"NB_TMA_STAGING": 1},
-    "tma_f64": {"NB_TMA_STAGING": 1},
+    "tma_t128": {"NB_TMA_STAGING": 1, "NB_F32_T": 128, "NB_F32_MINB": 1},
+    "tma_u8": {"NB_TMA_STAGING": 1, "NB_F32_UNROLL": 8},
+    "base2": {},
+    "tma2": {"NB_TMA_STAGING": 1},
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
