@@ -520,7 +520,7 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
 
   Core core;
   core.init(a.eps2, s_sums + tid, T);
-  uint32_t phase[2] = {0u, 0u};  // mbarrier phase parity per tile buffer (TMA staging)
+  uint32_t phase_bits = 0u;  // mbarrier phase parity of tile buffer b in bit b (TMA staging)
 
   for (int64_t u = u_begin; u < u_end;) {
     const int64_t b = u / NT;
@@ -584,8 +584,8 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
       const bool more = lo + TJ < s1;
       if (kTma) {
         if (more) issue_tile(buf ^ 1, lo + TJ);  // buf^1 was released by the last __syncthreads
-        mbar_wait(mbar + buf, phase[buf]);
-        phase[buf] ^= 1u;
+        mbar_wait(mbar + buf, (phase_bits >> buf) & 1u);
+        phase_bits ^= 1u << buf;
       } else if (more) {
         load_tile(lo + TJ);
       }
@@ -803,30 +803,36 @@ StepGeometry step_geometry(int64_t n_i, int64_t j_count) {
   return g;
 }
 
-// Persistent grid: SMs x resident CTAs per SM of the step kernels of one staging
-// mode (the smallest occupancy over the four variants, so every variant's grid
-// is fully resident).
-template <typename R>
-int max_grid(bool tma = false) {
-  static int cached[64][2] = {};
-  int dev = 0, sms = 0;
+// Persistent grid of a step kernel: SMs x its resident CTAs per SM (cached per
+// device and kernel).  NB_GRID_OVERRIDE=<ctas> replaces it (experiments).
+static int grid_for(const void* fn, int threads) {
+  struct Entry { int dev; const void* fn; int grid; };
+  static Entry cache[64];
+  static int used = 0;
+  int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) dev = 0;
-  if (cached[dev][tma]) return cached[dev][tma];
+  for (int k = 0; k < used; ++k)
+    if (cache[k].dev == dev && cache[k].fn == fn) return cache[k].grid;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int per_sm_min = 1 << 20;
-  for (int m = 0; m < 4; ++m) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fn<R>(m & 1, m & 2, tma), Cfg<R>::T, 0);
-    per_sm_min = per_sm < per_sm_min ? per_sm : per_sm_min;
-  }
-  int best = sms * (per_sm_min < 1 ? 1 : per_sm_min);
-  // Experiment hook: NB_GRID_OVERRIDE=<ctas> replaces the persistent grid size.
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+  int grid = sms * (per_sm < 1 ? 1 : per_sm);
   if (const char* env = getenv("NB_GRID_OVERRIDE")) {
     const int v = atoi(env);
-    if (v > 0) best = v;
+    if (v > 0) grid = v;
   }
-  cached[dev][tma] = best;
+  if (used < 64) cache[used++] = Entry{dev, fn, grid};
+  return grid;
+}
+
+// Largest persistent grid over every step-kernel variant of this precision
+// (sizes the stream-K slot workspace).
+template <typename R>
+int max_grid() {
+  int best = 1;
+  for (int m = 0; m < 8; ++m) {
+    const int g = grid_for(step_fn<R>(m & 1, m & 2, m & 4), Cfg<R>::T);
+    best = g > best ? g : best;
+  }
   return best;
 }
 
@@ -842,13 +848,14 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   a.n_iblocks = g.n_iblocks;
   a.units = g.units;
   const bool tma = use_tma<R>(a.n_i, a.j_count);
-  int grid = max_grid<R>(tma);
-  if ((int64_t)grid > g.units) grid = (int)g.units;
-  a.grid = grid;
   using C = Cfg<R>;
   constexpr int IB = C::T * C::template Core<false, false>::K;
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
+  const void* fn = step_fn<R>(mask_self, uni, tma);
+  int grid = grid_for(fn, C::T);
+  if ((int64_t)grid > g.units) grid = (int)g.units;
+  a.grid = grid;
 
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -861,7 +868,7 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* args[] = {&a};
-  cudaError_t e = cudaLaunchKernelExC(&cfg, step_fn<R>(mask_self, uni, tma), args);
+  cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
   count_launch();
   if (e != cudaSuccess) return e;
 
@@ -885,11 +892,11 @@ cudaError_t launch_simulate_persistent(StepArgs<R> a, int flags, V4<R>* pos_a, V
   a.n_tiles = g.n_tiles;
   a.n_iblocks = g.n_iblocks;
   a.units = g.units;
-  int grid = max_grid<R>(false);
-  if ((int64_t)grid > g.units) grid = (int)g.units;
-  a.grid = grid;
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
+  int grid = grid_for(step_fn<R>(mask_self, uni, false), Cfg<R>::T);
+  if ((int64_t)grid > g.units) grid = (int)g.units;
+  a.grid = grid;
   int any_split = 0;
   for (int64_t b = 0; b < g.n_iblocks && !any_split; ++b)
     any_split = host_cta_of(b * g.n_tiles, grid, g.units) != host_cta_of(b * g.n_tiles + g.n_tiles - 1, grid, g.units);
@@ -919,8 +926,7 @@ template <typename R>
 int64_t step_workspace_bytes(int64_t n_i) {
   const StepGeometry g = step_geometry<R>(n_i, 1);
   const int64_t counters = counters_bytes(g.n_iblocks);
-  const int64_t grid = max_grid<R>(false) > max_grid<R>(true) ? max_grid<R>(false) : max_grid<R>(true);
-  const int64_t slots = 2 * grid * 3 * g.i_block * 8;
+  const int64_t slots = 2 * (int64_t)max_grid<R>() * 3 * g.i_block * 8;
   return counters + slots;
 }
 
