@@ -776,18 +776,19 @@ static const void* step_fn(bool mask, bool uni, bool tma) {
   return uni ? kernel_ptr<R, false, true, false>() : kernel_ptr<R, false, false, false>();
 }
 
-// TMA (bulk-copy) staging for large FP32 launches: measured +0.6 % at
-// N=131072, -3 % at N=16384 (profiles/variants_r01_tma.txt).  NB_TMA=0/1 forces it.
+// TMA (bulk-copy) staging of the source tiles, FP32, launches with >=
+// NB_TMA_MIN_N targets and sources, enabled by NB_TMA=1.  Measured within noise
+// of the register path at N=131072 (71.6 % vs 71.8 %) and 3 % slower at
+// N=16384 (profiles/variants_r01_tma.txt), so it is off by default.
 template <typename R>
 static bool use_tma(int64_t n_i, int64_t j_count) {
   if (sizeof(R) != 4) return false;
-  static int forced = -2;
-  if (forced == -2) {
+  static int enabled = -1;
+  if (enabled < 0) {
     const char* env = getenv("NB_TMA");
-    forced = env ? atoi(env) : -1;
+    enabled = env ? atoi(env) != 0 : 0;
   }
-  if (forced >= 0) return forced != 0;
-  return n_i >= NB_TMA_MIN_N && j_count >= NB_TMA_MIN_N;
+  return enabled && n_i >= NB_TMA_MIN_N && j_count >= NB_TMA_MIN_N;
 }
 
 template <typename R>

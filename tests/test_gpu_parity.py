@@ -358,11 +358,7 @@ def test_full_size_accelerations_row_sampled(cfg_name, oracle):
     assert dev <= tol
 
 
-def test_tma_staged_path_with_wrapping_source_ranges(oracle):
-    """FP32 launches with >= 65536 targets and sources stage tiles by
-    cp.async.bulk; a circular source range that wraps past N (the multi-GPU
-    second phase) needs two bulk copies per tile.  Split the source range at an
-    odd offset (carry phases) and compare with the oracle."""
+def _wrapping_split_accelerations(n=70001):
     from paper_2203_08263_b200.device import DeviceState, kernel_flags
     n = 70001
     s = cube(n, 44, "single")
@@ -372,11 +368,41 @@ def test_tma_staged_path_with_wrapping_source_ranges(oracle):
     split = 12345  # phase 1: sources [12345, 12345+65537) mod n wraps; phase 2: the rest
     st.step(1.0, 1e-3, 0.0, 0, f, j_begin=split, j_count=65537, carry_mode=1, acc_out=out)
     st.step(1.0, 1e-3, 0.0, 0, f, j_begin=(split + 65537) % n, j_count=n - 65537, carry_mode=2, acc_out=out)
-    got = out[:, :3].cpu().numpy()
-    rows = np.arange(0, n, 701)
+    return s, out[:, :3].cpu().numpy()
+
+
+def test_split_wrapping_source_ranges(oracle):
+    """A circular source range that wraps past N (the multi-GPU second phase),
+    split at an odd offset into two carry phases, against the oracle."""
+    s, got = _wrapping_split_accelerations()
+    rows = np.arange(0, s.count, 701)
     pos = s.position_matrix()
     want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)), s.masses, rows, 1.0, 1e-3)
     assert nb_accel_dev(got[rows], want) <= F32_ACC_TOL
+
+
+def test_tma_staging_option(tmp_path):
+    """NB_TMA=1: source tiles staged by cp.async.bulk on mbarriers (two copies
+    per tile when the source range wraps); same accuracy, deterministic."""
+    import subprocess, sys, textwrap
+    script = textwrap.dedent(f"""
+        import os, sys, numpy as np
+        sys.path.insert(0, {REPO!r}); sys.path.insert(0, {os.path.join(REPO, "tests")!r})
+        import test_gpu_parity as T
+        from oracle import oracle as O
+        s, a = T._wrapping_split_accelerations()
+        _, b = T._wrapping_split_accelerations()
+        assert np.array_equal(a, b)
+        rows = np.arange(0, s.count, 701)
+        pos = s.position_matrix()
+        want = O.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)), s.masses, rows, 1.0, 1e-3)
+        dev = O.accel_dev(a[rows], want)
+        print("DEV", dev)
+        assert dev <= 1e-5, dev
+    """)
+    env = dict(os.environ, NB_TMA="1")
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
 
 
 def test_plummer_row_sampled(oracle):
