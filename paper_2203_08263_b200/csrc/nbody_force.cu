@@ -72,13 +72,13 @@
 #define NB_F64_K 6
 #endif
 #ifndef NB_F64_T
-#define NB_F64_T 128
+#define NB_F64_T 256
 #endif
 #ifndef NB_F64_TJ
-#define NB_F64_TJ 128
+#define NB_F64_TJ 256
 #endif
 #ifndef NB_F64_MINB
-#define NB_F64_MINB 2
+#define NB_F64_MINB 1
 #endif
 #ifndef NB_F64_UNROLL
 #define NB_F64_UNROLL 8

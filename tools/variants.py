@@ -14,11 +14,11 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "tma": {"NB_TMA_STAGING": 1},
-    "tma_t128": {"NB_TMA_STAGING": 1, "NB_F32_T": 128, "NB_F32_MINB": 1},
-    "tma_u8": {"NB_TMA_STAGING": 1, "NB_F32_UNROLL": 8},
-    "base2": {},
-    "tma2": {"NB_TMA_STAGING": 1},
+    "f64_t256_tj256": {"NB_F64_T": 256, "NB_F64_TJ": 256, "NB_F64_MINB": 1},
+    "f64_t256_tj256_k4": {"NB_F64_T": 256, "NB_F64_TJ": 256, "NB_F64_MINB": 1, "NB_F64_K": 4},
+    "f64_t256_tj256_u16": {"NB_F64_T": 256, "NB_F64_TJ": 256, "NB_F64_MINB": 1, "NB_F64_UNROLL": 16},
+    "f64_k6_nsw": {"NB_F64_STAGEWISE": 0},
+    "f64_k8_minb1": {"NB_F64_K": 8, "NB_F64_MINB": 1},
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
