@@ -405,6 +405,33 @@ def test_tma_staging_option(tmp_path):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
 
 
+@pytest.mark.parametrize("cfg_name", ["C2", "C3-f32", "C3-f64"])
+def test_full_size_trajectory_vs_oracle(cfg_name, oracle):
+    """SURVEY.md 8(c) trajectory tolerances at full BASELINE size: the whole
+    simulate against the FP64 oracle port (all host cores) on the same rounded
+    inputs -- FP64 within 1e-12; FP32 within 10x the reference's own FP32-vs-FP64
+    deviation (the reference's recip-form FP32 run, reproduced bit for bit by the
+    port)."""
+    cfg = nb.BASELINE_CONFIGS[cfg_name]
+    s = cfg.system()
+    p = cfg.params()
+    fin = nb.simulate(s, p).position_matrix()
+    pos64 = s.position_matrix()
+    vel64 = np.stack(s.velocities, 1).astype(np.float64)
+    th = oracle.host_threads()
+    ref64, _ = oracle.simulate(pos64, vel64, s.masses.astype(np.float64), 1.0, p.dt, p.softening_sq, p.steps,
+                               threads=th)
+    dev = oracle.position_dev(fin, ref64)
+    if cfg.precision is nb.Precision.DOUBLE:
+        assert dev <= F64_POS_TOL, dev
+    else:
+        ref32, _ = oracle.simulate(np.stack(s.positions, 1), np.stack(s.velocities, 1), s.masses, 1.0, p.dt,
+                                   p.softening_sq, p.steps, threads=th)
+        ref_dev = oracle.position_dev(ref32, ref64)
+        print(cfg_name, "gpu", dev, "reference fp32", ref_dev)
+        assert dev <= 10 * ref_dev, (dev, ref_dev)
+
+
 def test_plummer_row_sampled(oracle):
     """C5's distribution (Plummer, equal masses) at 1/16 of its N."""
     s = nb.plummer_sphere(262144, 0, nb.Precision.SINGLE)
