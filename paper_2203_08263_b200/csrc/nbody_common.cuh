@@ -63,6 +63,16 @@ __device__ __forceinline__ float rsqrt_mufu(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float lg2_mufu(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_mufu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 // Bare MUFU.RSQ64H seed (about 2^-22 relative); refined by the caller.
 __device__ __forceinline__ double rsqrt_seed(double x) {
   double y;

@@ -62,6 +62,11 @@
 #ifndef NB_F32_STAGEWISE
 #define NB_F32_STAGEWISE 0
 #endif
+#ifndef NB_F32_EXP2_MASK
+// Which (target pair q, source parity p) weights go through MUFU.LG2/EX2 instead
+// of MUFU.RSQ + FMUL2s: bit q + (K/2)*p.  0 = none.
+#define NB_F32_EXP2_MASK 17  // pair 0 on even sources, pair 1 on odd: 1/3 of the weights (measured best)
+#endif
 #ifndef NB_TMA_MIN_N
 #define NB_TMA_MIN_N 65536  // FP32 launches with >= this many targets and sources use TMA staging
 #endif
@@ -179,6 +184,9 @@ struct CoreF32 {
   using R = float;
   static constexpr int K = K_;
   static constexpr int KP = K / 2;
+  static constexpr unsigned XMASK = NB_F32_EXP2_MASK & ((1u << (2 * KP)) - 1u);  // LG2/EX2 weights
+  static constexpr bool NEEDS_LM = XMASK != 0 && !UNI;  // needs log2(m_j) per source
+  const float* lmt;  // this tile's log2(m_j) (NEEDS_LM)
 #if NB_F32_SUMS_IN_REGS
   static constexpr int SMEM_SUMS = 1;
   double rs[3 * K];  // FP64 segment sums in registers (1 CTA/SM leaves room)
@@ -228,11 +236,21 @@ struct CoreF32 {
   // order): consecutive instructions share the broadcast source operand, and the
   // accumulate -- the instruction with three distinct register pairs, which the
   // register file cannot feed at full rate -- gets the most reuse.
-  __device__ __forceinline__ f2x weight(f2x d2, f2x mj, int jj, int q) const {
+  __device__ __forceinline__ f2x weight(f2x d2, f2x mj, f2x lmj, int jj, int q) const {
     float d2a, d2b;
     upk(d2, d2a, d2b);
     f2x w;
 #if NB_F32_MATH == 0
+    if ((XMASK >> (q + KP * (jj & 1))) & 1u) {
+      // m d2^(-3/2) = 2^(-1.5 log2 d2 + log2 m): one FFMA2 and four MUFU ops in
+      // place of three FMUL2 + two MUFU.RSQ -- moves FP32-pipe work onto the XU
+      // pipe, which the rsqrt form leaves ~40 % idle.
+      const f2x l = pk(lg2_mufu(d2a), lg2_mufu(d2b));
+      const f2x e = UNI ? mul2(l, pk(-1.5f, -1.5f)) : fma2(l, pk(-1.5f, -1.5f), lmj);
+      float ea, eb;
+      upk(e, ea, eb);
+      w = pk(ex2_mufu(ea), ex2_mufu(eb));
+    } else {
     const f2x r = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
     // r^2 by FMUL2.  (Taking it from MUFU.RCP for some pairs, to shift work to
     // the XU pipe, was measured slower: the XU pipe saturates first.)
@@ -240,6 +258,7 @@ struct CoreF32 {
     // UNI (all masses equal): m is applied once to the finished sum, saving
     // one FMUL2 of 12 per interaction pair.
     w = UNI ? mul2(r2, r) : mul2(mul2(r, mj), r2);
+    }
 #else
     float ma, mb;
     upk(mj, ma, mb);
@@ -257,6 +276,9 @@ struct CoreF32 {
 
   __device__ __forceinline__ void interact(const F4& pj, int jj) {
     const f2x xj = pk(pj.x, pj.x), yj = pk(pj.y, pj.y), zj = pk(pj.z, pj.z), mj = pk(pj.w, pj.w);
+    float lm = 0.f;
+    if (NEEDS_LM) lm = lmt[jj];
+    const f2x lmj = pk(lm, lm);
 #if !NB_F32_STAGEWISE
 #pragma unroll
     for (int q = 0; q < KP; ++q) {  // ladder rung: per-pair order
@@ -264,7 +286,7 @@ struct CoreF32 {
       f2x d2 = fma2(dx, dx, e2);
       d2 = fma2(dy, dy, d2);
       d2 = fma2(dz, dz, d2);
-      const f2x w = weight(d2, mj, jj, q);
+      const f2x w = weight(d2, mj, lmj, jj, q);
       tx[q] = fma2(dx, w, tx[q]);
       ty[q] = fma2(dy, w, ty[q]);
       tz[q] = fma2(dz, w, tz[q]);
@@ -284,7 +306,7 @@ struct CoreF32 {
 #pragma unroll
     for (int q = 0; q < KP; ++q) d2[q] = fma2(dz[q], dz[q], d2[q]);
 #pragma unroll
-    for (int q = 0; q < KP; ++q) w[q] = weight(d2[q], mj, jj, q);
+    for (int q = 0; q < KP; ++q) w[q] = weight(d2[q], mj, lmj, jj, q);
 #pragma unroll
     for (int q = 0; q < KP; ++q) {
       tx[q] = fma2(w[q], dx[q], tx[q]);
@@ -324,6 +346,8 @@ struct CoreF64 {
   using R = double;
   static constexpr int K = K_;
   static constexpr int SMEM_SUMS = 1;
+  static constexpr bool NEEDS_LM = false;
+  const float* lmt;
   double nx[K], ny[K], nz[K];
   double sx[K], sy[K], sz[K];
   int selfj[K];
@@ -521,6 +545,7 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
   Core core;
   core.init(a.eps2, s_sums + tid, T);
   uint32_t phase_bits = 0u;  // mbarrier phase parity of tile buffer b in bit b (TMA staging)
+  __shared__ float tile_lm[2][Core::NEEDS_LM ? TJ : 1];  // log2(m_j) of the staged tiles
 
   for (int64_t u = u_begin; u < u_end;) {
     const int64_t b = u / NT;
@@ -568,7 +593,10 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
     };
     auto store_tile = [&](int buf) {
 #pragma unroll
-      for (int r = 0; r < PER; ++r) tile[buf][r * T + tid] = stage[r];
+      for (int r = 0; r < PER; ++r) {
+        tile[buf][r * T + tid] = stage[r];
+        if (Core::NEEDS_LM) tile_lm[buf][r * T + tid] = lg2_mufu((float)stage[r].w);
+      }
     };
 
     if (kTma) {
@@ -586,6 +614,11 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
         if (more) issue_tile(buf ^ 1, lo + TJ);  // buf^1 was released by the last __syncthreads
         mbar_wait(mbar + buf, (phase_bits >> buf) & 1u);
         phase_bits ^= 1u << buf;
+        if (Core::NEEDS_LM) {
+#pragma unroll
+          for (int r = 0; r < PER; ++r) tile_lm[buf][r * T + tid] = lg2_mufu((float)tile[buf][r * T + tid].w);
+          __syncthreads();
+        }
       } else if (more) {
         load_tile(lo + TJ);
       }
@@ -601,6 +634,7 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
         }
       }
       core.begin_tile();
+      core.lmt = tile_lm[buf];
       const B* tb = tile[buf];
       if (count == TJ) {
         core.template full_tile<TJ>(tb);

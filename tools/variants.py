@@ -14,11 +14,8 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "f64_t256_tj256": {"NB_F64_T": 256, "NB_F64_TJ": 256, "NB_F64_MINB": 1},
-    "f64_t256_tj256_k4": {"NB_F64_T": 256, "NB_F64_TJ": 256, "NB_F64_MINB": 1, "NB_F64_K": 4},
-    "f64_t256_tj256_u16": {"NB_F64_T": 256, "NB_F64_TJ": 256, "NB_F64_MINB": 1, "NB_F64_UNROLL": 16},
-    "f64_k6_nsw": {"NB_F64_STAGEWISE": 0},
-    "f64_k8_minb1": {"NB_F64_K": 8, "NB_F64_MINB": 1},
+    "m0": {"NB_F32_EXP2_MASK": 0},     # rsqrt weights only
+    "m9": {"NB_F32_EXP2_MASK": 9},     # pair 0, every source (f = 1/3)
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
@@ -26,19 +23,24 @@ VARIANTS = {
 # onto GPU knobs, each rung adding one change to the previous one (FP32, C3).
 LADDER = [
     ("L0 pow form, scalar FP32, K=2, no unroll, per-pair order",
-     {"NB_F32_MATH": 2, "NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_UNROLL": 1, "NB_F32_STAGEWISE": 0}),
+     {"NB_F32_MATH": 2, "NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_UNROLL": 1, "NB_F32_STAGEWISE": 0,
+      "NB_F32_EXP2_MASK": 0}),
     ("L1 + recip form (reference's fastest CPU rung)",
-     {"NB_F32_MATH": 1, "NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_UNROLL": 1, "NB_F32_STAGEWISE": 0}),
+     {"NB_F32_MATH": 1, "NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_UNROLL": 1, "NB_F32_STAGEWISE": 0,
+      "NB_F32_EXP2_MASK": 0}),
     ("L2 + MUFU rsqrt form",
-     {"NB_F32_MATH": 0, "NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_UNROLL": 1, "NB_F32_STAGEWISE": 0}),
+     {"NB_F32_MATH": 0, "NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_UNROLL": 1, "NB_F32_STAGEWISE": 0,
+      "NB_F32_EXP2_MASK": 0}),
     ("L3 + unrolled source loop (x16)",
-     {"NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_STAGEWISE": 0}),
+     {"NB_F32_PACKED": 0, "NB_F32_K": 2, "NB_F32_STAGEWISE": 0, "NB_F32_EXP2_MASK": 0}),
     ("L4 + register blocking, 6 targets/thread",
-     {"NB_F32_PACKED": 0, "NB_F32_STAGEWISE": 0}),
-    ("L5 + packed FFMA2/FADD2/FMUL2 (shipped)", {}),
-    ("L5' (alternative) stage-wise source order across the pairs", {"NB_F32_STAGEWISE": 1}),
+     {"NB_F32_PACKED": 0, "NB_F32_STAGEWISE": 0, "NB_F32_EXP2_MASK": 0}),
+    ("L5 + packed FFMA2/FADD2/FMUL2", {"NB_F32_EXP2_MASK": 0}),
+    ("L6 + 1/3 of the weights via MUFU.LG2/EX2 (shipped)", {}),
+    ("L6' (alternative) stage-wise source order across the pairs", {"NB_F32_STAGEWISE": 1}),
 ]
-# VARIANTS.update({f"ladder{i}": d for i, (_, d) in enumerate(LADDER)})  # enable for the ladder run
+if os.environ.get("NB_LADDER"):  # NB_LADDER=1 python tools/variants.py build|run C3-f32
+    VARIANTS.update({f"ladder{i}": d for i, (_, d) in enumerate(LADDER)})
 
 
 def build_one(name, defs):
@@ -95,7 +97,10 @@ def run(configs):
         ref_state = DeviceState(s.position_matrix().astype(dt), np.stack(s.velocities, 1), s.masses, dt)
         mask = kernel_flags(s.masses, cfg.softening_sq, dt)
         ref_acc = ref_state.accelerations(1.0, cfg.softening_sq, mask).cpu().numpy().astype(np.float64)
+        only = [v for v in os.environ.get("NB_VARIANTS", "").split(",") if v]
         for name in VARIANTS:
+            if only and name not in only:
+                continue
             path = os.path.join(OUT, f"lib_{name}.so")
             if not os.path.exists(path):
                 continue
