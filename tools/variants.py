@@ -14,8 +14,10 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "m0": {"NB_F32_EXP2_MASK": 0},     # rsqrt weights only
-    "m9": {"NB_F32_EXP2_MASK": 9},     # pair 0, every source (f = 1/3)
+    "tail16": {"NB_TAIL16": 1},
+    "fix8": {"NB_FIXUP_BATCH": 8},
+    "fix16": {"NB_FIXUP_BATCH": 16},
+    "tail16_fix8": {"NB_TAIL16": 1, "NB_FIXUP_BATCH": 8},
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
