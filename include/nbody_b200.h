@@ -186,6 +186,17 @@ int nb_dev_simulate_timed_f64(void* pos4_a, void* pos4_b, void* vel4, void* acc4
                               void* workspace, int64_t workspace_bytes, void* stream,
                               int* final_in_b, float* launch_ms);
 
+/* Boundary layout conversion on the device: the caller's
+ * SoA columns (one contiguous H2D) into the packed rows, and back (one
+ * contiguous D2H).  pack: out4[i] = (x[i], y[i], z[i], w ? w[i] : 0);
+ * unpack: x[i], y[i], z[i] = in4[i].xyz.  All device pointers, n entries. */
+int nb_dev_pack_f32(const void* x, const void* y, const void* z, const void* w, int64_t n,
+                    void* out4, void* stream);
+int nb_dev_pack_f64(const void* x, const void* y, const void* z, const void* w, int64_t n,
+                    void* out4, void* stream);
+int nb_dev_unpack_f32(const void* in4, int64_t n, void* x, void* y, void* z, void* stream);
+int nb_dev_unpack_f64(const void* in4, int64_t n, void* x, void* y, void* z, void* stream);
+
 /* Stand-alone update kernels on packed arrays (n entries each): the kick-drift
  * of step_soa (_accel_cy.pyx:205-237) in place, and the trapezoidal kick of
  * _kick (kernels/__init__.py:220-227): v += (a_new - a_old) * real(factor). */

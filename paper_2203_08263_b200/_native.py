@@ -44,6 +44,8 @@ _ARGTYPES = {
     "nb_dev_simulate": [_p, _p, _p, _p, _i64, _d, _d, _d, _i64, _i, _p, _i64, _p, ctypes.POINTER(_i)],
     "nb_dev_simulate_timed": [_p, _p, _p, _p, _i64, _d, _d, _d, _i64, _i, _p, _i64, _p, ctypes.POINTER(_i),
                               ctypes.POINTER(ctypes.c_float)],
+    "nb_dev_pack": [_p, _p, _p, _p, _i64, _p, _p],
+    "nb_dev_unpack": [_p, _i64, _p, _p, _p, _p],
     "nb_dev_drift": [_p, _p, _p, _i64, _d, _p],
     "nb_dev_kick": [_p, _p, _p, _i64, _d, _p],
     "nb_dev_energy": [_p, _p, _i64, _d, _d, _p, _p, _i64, _p],

@@ -369,6 +369,29 @@ int host_simulate(R* px, R* py, R* pz, R* vx, R* vy, R* vz, const R* m, int64_t 
 }
 
 template <typename R>
+int dev_pack(const void* x, const void* y, const void* z, const void* w, int64_t n, void* out4, void* stream) {
+  if (n < 0) return fail(NB_ERR_ARG, "n must be >= 0");
+  if (n == 0) return NB_OK;
+  if (!x || !y || !z || !out4) return fail(NB_ERR_ARG, "null device pointer");
+  if (cudaError_t be = bind_device_of(out4)) return cuda_fail(be, "out4 is not a device pointer");
+  NB_CUDA(launch_pack_soa<R>(static_cast<const R*>(x), static_cast<const R*>(y), static_cast<const R*>(z),
+                             static_cast<const R*>(w), static_cast<V4<R>*>(out4), n,
+                             static_cast<cudaStream_t>(stream)));
+  return NB_OK;
+}
+
+template <typename R>
+int dev_unpack(const void* in4, int64_t n, void* x, void* y, void* z, void* stream) {
+  if (n < 0) return fail(NB_ERR_ARG, "n must be >= 0");
+  if (n == 0) return NB_OK;
+  if (!in4 || !x || !y || !z) return fail(NB_ERR_ARG, "null device pointer");
+  if (cudaError_t be = bind_device_of(in4)) return cuda_fail(be, "in4 is not a device pointer");
+  NB_CUDA(launch_unpack_soa<R>(static_cast<const V4<R>*>(in4), static_cast<R*>(x), static_cast<R*>(y),
+                               static_cast<R*>(z), n, static_cast<cudaStream_t>(stream)));
+  return NB_OK;
+}
+
+template <typename R>
 int dev_drift(void* pos4, void* vel4, const void* acc4, int64_t n, double dt, void* stream) {
   if (n < 0) return fail(NB_ERR_ARG, "n must be >= 0");
   if (n == 0) return NB_OK;
@@ -516,6 +539,20 @@ int nb_dev_simulate_timed_f64(void* pos4_a, void* pos4_b, void* vel4, void* acc4
                               void* stream, int* final_in_b, float* launch_ms) {
   return dev_simulate_timed<double>(pos4_a, pos4_b, vel4, acc4, n, g, dt, eps2, steps, flags, workspace,
                                     workspace_bytes, stream, final_in_b, launch_ms);
+}
+int nb_dev_pack_f32(const void* x, const void* y, const void* z, const void* w, int64_t n, void* out4,
+                    void* stream) {
+  return dev_pack<float>(x, y, z, w, n, out4, stream);
+}
+int nb_dev_pack_f64(const void* x, const void* y, const void* z, const void* w, int64_t n, void* out4,
+                    void* stream) {
+  return dev_pack<double>(x, y, z, w, n, out4, stream);
+}
+int nb_dev_unpack_f32(const void* in4, int64_t n, void* x, void* y, void* z, void* stream) {
+  return dev_unpack<float>(in4, n, x, y, z, stream);
+}
+int nb_dev_unpack_f64(const void* in4, int64_t n, void* x, void* y, void* z, void* stream) {
+  return dev_unpack<double>(in4, n, x, y, z, stream);
 }
 int nb_dev_drift_f32(void* pos4, void* vel4, const void* acc4, int64_t n, double dt, void* stream) {
   return dev_drift<float>(pos4, vel4, acc4, n, dt, stream);

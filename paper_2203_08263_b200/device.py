@@ -92,11 +92,7 @@ class DeviceState:
         self.sfx = "_f32" if self.dtype == np.float32 else "_f64"
         self.pbytes = self.dtype.itemsize
         tdt = TORCH_DTYPE[self.dtype]
-        # pinned staging, reused by every load()/readback of this state
-        self._h_pos = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
-        self._h_vel = torch.empty((max(self.n_i, 1), 4), dtype=tdt, pin_memory=True)
-        self._h_out = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
-        self._h2d_done = None
+        self._alloc_staging()
         if pos_buffer is not None:
             # caller-provided (2, N, 4) storage, e.g. symmetric memory peers can write into
             if tuple(pos_buffer.shape) != (2, self.n, 4) or pos_buffer.dtype != tdt:
@@ -113,30 +109,70 @@ class DeviceState:
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.load(positions, velocities, masses)
 
+    def _alloc_staging(self) -> None:
+        """Column staging reused by every load()/readback: 7 columns (x, y, z, m of
+        all N bodies; vx, vy, vz of the n_i owned ones) in pinned host memory and on
+        the device, so each transfer is ONE contiguous copy and the (de)interleave
+        to the packed rows runs on the GPU (nb_dev_pack / nb_dev_unpack)."""
+        tdt = TORCH_DTYPE[self.dtype]
+        ncol = 4 * self.n + 3 * max(self.n_i, 1)
+        self._h_cols = torch.empty(ncol, dtype=tdt, pin_memory=True)
+        self._d_cols = torch.empty(ncol, dtype=tdt, device=self.device)
+        self._h_out = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
+        self._h2d_done = None
+
+    def _col(self, t: torch.Tensor, k: int) -> int:
+        """Device/host address of staging column k (0-3: x, y, z, m; 4-6: vx, vy, vz)."""
+        off = k * self.n if k < 4 else 4 * self.n + (k - 4) * max(self.n_i, 1)
+        return t.data_ptr() + off * self.pbytes
+
     def load(self, positions, velocities, masses: np.ndarray) -> None:
         """(Re)initialise the resident state from host data -- (N,3) arrays or
-        (x, y, z) column tuples -- through the pinned staging and an asynchronous
-        H2D on the current stream; buffers are reused."""
+        (x, y, z) column tuples: contiguous column writes into the pinned staging,
+        one asynchronous H2D and two pack launches on the current stream."""
         if self._h2d_done is not None:
             self._h2d_done.synchronize()  # staging still feeding the previous copy
         self.masses = np.ascontiguousarray(masses, dtype=self.dtype)
-        hp = self._h_pos.numpy()
-        hv = self._h_vel.numpy()
-        lo, hi = self.i_begin, self.i_begin + self.n_i
-        if isinstance(positions, (tuple, list)):
-            for k in range(3):
-                hp[:, k] = positions[k]
-                hv[: self.n_i, k] = velocities[k][lo:hi]
-        else:
-            hp[:, :3] = positions
-            hv[: self.n_i, :3] = np.asarray(velocities)[lo:hi]
-        hp[:, 3] = self.masses
-        hv[:, 3] = 0
-        self.pos_a.copy_(self._h_pos, non_blocking=True)
-        self.vel.copy_(self._h_vel, non_blocking=True)
+        n, ni = self.n, self.n_i
+        h = self._h_cols.numpy()
+        lo, hi = self.i_begin, self.i_begin + ni
+        if not isinstance(positions, (tuple, list)):
+            positions = tuple(np.asarray(positions)[:, k] for k in range(3))
+            velocities = tuple(np.asarray(velocities)[:, k] for k in range(3))
+        for k in range(3):
+            h[k * n:(k + 1) * n] = positions[k]
+            h[4 * n + k * max(ni, 1): 4 * n + k * max(ni, 1) + ni] = velocities[k][lo:hi]
+        h[3 * n:4 * n] = self.masses
+        self._d_cols.copy_(self._h_cols, non_blocking=True)
         self._h2d_done = torch.cuda.Event()
         self._h2d_done.record()
+        d, s = self._d_cols, self.stream_ptr()
+        _native.call("nb_dev_pack" + self.sfx, self._col(d, 0), self._col(d, 1), self._col(d, 2),
+                     self._col(d, 3), n, self.pos_a.data_ptr(), s)
+        if ni:
+            _native.call("nb_dev_pack" + self.sfx, self._col(d, 4), self._col(d, 5), self._col(d, 6), None, ni,
+                         self.vel.data_ptr(), s)
         self.cur_is_a = True
+
+    def columns_host(self):
+        """Current positions (x, y, z of all N) and velocities (of the n_i owned
+        rows) as six fresh contiguous host arrays: two unpack launches, one
+        contiguous D2H into the pinned staging, six memcpys."""
+        d, s = self._d_cols, self.stream_ptr()
+        n, ni = self.n, self.n_i
+        _native.call("nb_dev_unpack" + self.sfx, self.pos_cur.data_ptr(), n, self._col(d, 0), self._col(d, 1),
+                     self._col(d, 2), s)
+        if ni:
+            _native.call("nb_dev_unpack" + self.sfx, self.vel.data_ptr(), ni, self._col(d, 4), self._col(d, 5),
+                         self._col(d, 6), s)
+        if self._h2d_done is not None:
+            self._h2d_done.synchronize()
+            self._h2d_done = None
+        self._h_cols.copy_(self._d_cols)  # synchronizes the stream
+        h = self._h_cols.numpy()
+        pos = tuple(np.array(h[k * n:(k + 1) * n]) for k in range(3))
+        vel = tuple(np.array(h[4 * n + k * max(ni, 1): 4 * n + k * max(ni, 1) + ni]) for k in range(3))
+        return pos, vel
 
     @classmethod
     def from_generator(cls, kind: str, n: int, seed: int, dtype,
@@ -161,10 +197,7 @@ class DeviceState:
         _native.call("nb_dev_init" + self.sfx, codes[kind], int(seed), self.n, self.pos_a.data_ptr(),
                      self.vel.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
         self.masses = None  # device-resident only; see masses_host()
-        self._h_pos = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
-        self._h_vel = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
-        self._h_out = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
-        self._h2d_done = None
+        self._alloc_staging()
         self.acc = torch.empty((self.n, 4), dtype=tdt, device=self.device)
         self.carry = torch.empty((3, self.n), dtype=torch.float64, device=self.device)
         self.ws_bytes = _native.workspace_bytes(self.pbytes, self.n)
@@ -264,11 +297,9 @@ class DeviceState:
         return self._h_out.numpy()
 
     def velocities_packed(self) -> np.ndarray:
-        h = self._h_vel_out if hasattr(self, "_h_vel_out") else None
-        if h is None:
-            self._h_vel_out = h = torch.empty_like(self._h_vel)
-        h.copy_(self.vel)
-        return h.numpy()[: self.n_i]
+        """(n_i, 4) pinned view of the owned velocities; valid until the next readback."""
+        self._h_out[: self.vel.shape[0]].copy_(self.vel)
+        return self._h_out.numpy()[: self.n_i]
 
     def positions_host(self) -> np.ndarray:
         """Current positions (N, 3): one D2H of the packed rows into pinned memory."""

@@ -297,19 +297,17 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
         _store(state, "positions", pos)
         _store(state, "velocities", vel)
         return state
-    # Single GPU: columns go straight into the pinned staging of the resident
-    # state and the result arrays are cut straight from the pinned readback.
+    # Single GPU: columns go straight into the pinned column staging of the
+    # resident state (one H2D, packed on the device) and the result columns come
+    # back unpacked on the device in one D2H.
     from .device import kernel_flags
     m = np.asarray(sys_.masses, dtype)
     st = _resident_state(_columns(sys_, "positions"), _columns(sys_, "velocities"), m, dtype)
     st.simulate(params.gravitational_constant, params.dt, params.softening_sq, params.steps,
                 kernel_flags(m, params.softening_sq, dtype))
-    hp = st.positions_packed()
-    pos = tuple(np.ascontiguousarray(hp[:, k]) for k in range(3))
-    hv = st.velocities_packed()
-    vel = tuple(np.ascontiguousarray(hv[:, k]) for k in range(3))
+    pos, vel = st.columns_host()
     if _value(sys_.layout) != "soa":
-        pos, vel = np.ascontiguousarray(hp[:, :3]), np.ascontiguousarray(hv[:, :3])
+        pos, vel = np.stack(pos, 1), np.stack(vel, 1)
     return type(sys_)(sys_.layout, sys_.precision, pos, vel, sys_.masses.copy())
 
 
