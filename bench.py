@@ -119,7 +119,7 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- CPU baseline
 
-def cpu_reference_rate(cfg, sys0, budget_s: float = 20.0, fixed_n: int = 0):
+def cpu_reference_rate(cfg, sys0, fixed_n: int = 0, reps: int = 2, warm: bool = True):
     """Reference CPU path on this host: the reference's compiled accel_soa
     (oracle/_ref) over all host threads, soa-recip (its fastest rung), on the
     config's state.  Returns (interactions/s, description dict)."""
@@ -141,10 +141,13 @@ def cpu_reference_rate(cfg, sys0, budget_s: float = 20.0, fixed_n: int = 0):
 
         def run():
             O.accel_soa(cols[0], cols[1], cols[2], m, 1.0, cfg.softening_sq, True, 0, threads)
+    if warm:
+        run()  # warm-up: OpenMP team, page faults, clock ramp
     t0 = time.perf_counter()
-    run()
-    t = time.perf_counter() - t0
-    return float(n) * n / t, {"kind": kind, "cores": threads, "seconds": t, "n": n}
+    for _ in range(reps):
+        run()
+    t = (time.perf_counter() - t0) / reps
+    return float(n) * n / t, {"kind": kind, "cores": threads, "seconds": t, "n": n, "reps": reps}
 
 
 def cpu_rate_isolated(cfg_name: str, fixed_n: int = 0):
@@ -388,9 +391,10 @@ def run_ours(args) -> dict:
             what = "the reference's compiled accel_soa" if desc["kind"] == "reference" else "the oracle C port"
             result["cpu_baseline"] = {
                 "value": rate, "unit": UNIT, "cores": desc["cores"], "kind": desc["kind"],
-                "sample": f"one force evaluation (N^2 = {desc['n'] ** 2:.3e} interactions) of the "
-                          f"{cfg.name} initial state through {what} "
-                          f"(soa-recip, {desc['cores']} threads), {desc['seconds']:.2f} s"}
+                "sample": f"mean of {desc['reps']} force evaluations (N^2 = {desc['n'] ** 2:.3e} "
+                          f"interactions each, after one warm-up evaluation) of the {cfg.name} initial "
+                          f"state through {what} (soa-recip, {desc['cores']} threads), "
+                          f"{desc['seconds']:.2f} s each"}
     if world > 1:
         dist.destroy_process_group()
     return result if rank == 0 else None
@@ -422,10 +426,10 @@ def run_reference(args) -> dict:
         n_s = int(cfg.n * (budget / (per_step * (args.steps + args.warmup))) ** 0.5) // 1024 * 1024
         n_s = max(n_s, 4096)
     for _ in range(args.warmup):
-        cpu_reference_rate(cfg, sys0, fixed_n=n_s)
+        cpu_reference_rate(cfg, sys0, fixed_n=n_s, reps=1, warm=False)
     total, inter = 0.0, 0.0
     for _ in range(args.steps):
-        r, d = cpu_reference_rate(cfg, sys0, fixed_n=n_s)
+        r, d = cpu_reference_rate(cfg, sys0, fixed_n=n_s, reps=1, warm=False)
         total += d["seconds"]
         inter += float(n_s) * n_s
     value = inter / total
