@@ -14,10 +14,10 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "tail16": {"NB_TAIL16": 1},
-    "fix8": {"NB_FIXUP_BATCH": 8},
-    "fix16": {"NB_FIXUP_BATCH": 16},
-    "tail16_fix8": {"NB_TAIL16": 1, "NB_FIXUP_BATCH": 8},
+    "prev": {},  # HEAD before the segment refactor (built from a stash)
+    "noinl": {"NB_SEG_NOINLINE": 1},
+    "noinl_u8": {"NB_SEG_NOINLINE": 1, "NB_F32_UNROLL": 8},
+    "noresize_noinl": {"NB_SEG_NOINLINE": 1, "NB_RESIZE_LAST": 0},
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
