@@ -14,10 +14,10 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "prev": {},  # HEAD before the segment refactor (built from a stash)
-    "noinl": {"NB_SEG_NOINLINE": 1},
-    "noinl_u8": {"NB_SEG_NOINLINE": 1, "NB_F32_UNROLL": 8},
-    "noresize_noinl": {"NB_SEG_NOINLINE": 1, "NB_RESIZE_LAST": 0},
+    "u8": {"NB_F32_UNROLL": 8},
+    "u12": {"NB_F32_UNROLL": 12},
+    "u4": {"NB_F32_UNROLL": 4},
+    "u32": {"NB_F32_UNROLL": 32},
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
