@@ -212,7 +212,11 @@ int nb_dev_kick_f64(void* vel4, const void* acc4_new, const void* acc4_old, int6
 /* Softened potential energy  -G * sum_{i<j} m_i m_j / sqrt(|p_i-p_j|^2 + eps2)
  * and kinetic energy / momentum of the packed state (validation.py:134-145),
  * accumulated in FP64.  out6 (device, 6 doubles) <- (KE, PE, Px, Py, Pz, KE+PE).
- * workspace: device scratch of at least 8*n bytes (per-body potentials). */
+ * workspace: device scratch of at least 8*n bytes (per-body potentials);
+ * nb_energy_workspace_bytes(precision_bytes, n) is the size that lets the pass
+ * split the sources into ranges (to fill the GPU at any N) and reduce on every
+ * SM.  The reduction order is fixed for a given device and workspace size. */
+int64_t nb_energy_workspace_bytes(int precision_bytes, int64_t n);
 int nb_dev_energy_f32(const void* pos4, const void* vel4, int64_t n, double g, double eps2,
                       double* out6, void* workspace, int64_t workspace_bytes, void* stream);
 int nb_dev_energy_f64(const void* pos4, const void* vel4, int64_t n, double g, double eps2,

@@ -78,6 +78,8 @@ def lib() -> ctypes.CDLL:
                 fn.restype = _i
         L.nb_dev_workspace_bytes.argtypes = [_i, _i64]
         L.nb_dev_workspace_bytes.restype = _i64
+        L.nb_energy_workspace_bytes.argtypes = [_i, _i64]
+        L.nb_energy_workspace_bytes.restype = _i64
         L.nb_last_error.restype = ctypes.c_char_p
         L.nb_version.restype = ctypes.c_char_p
         L.nb_launch_count.restype = _i64
@@ -92,6 +94,10 @@ def call(name: str, *args) -> None:
     if rc != 0:
         msg = L.nb_last_error()
         raise NativeError(name, rc, msg.decode() if msg else "")
+
+
+def energy_workspace_bytes(precision_bytes: int, n: int) -> int:
+    return int(lib().nb_energy_workspace_bytes(precision_bytes, n))
 
 
 def workspace_bytes(precision_bytes: int, n_i: int) -> int:

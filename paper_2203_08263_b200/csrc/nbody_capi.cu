@@ -421,7 +421,7 @@ int dev_energy(const void* pos4, const void* vel4, int64_t n, double g, double e
   if (cudaError_t be = bind_device_of(pos4)) return cuda_fail(be, "pos4 is not a device pointer");
   if (!ws || ws_bytes < 8 * n) return fail(NB_ERR_WORKSPACE, "energy needs a workspace of 8*n bytes");
   NB_CUDA(launch_energy<R>(static_cast<const V4<R>*>(pos4), static_cast<const V4<R>*>(vel4), n, g, eps2, out6,
-                           static_cast<double*>(ws), static_cast<cudaStream_t>(stream)));
+                           static_cast<double*>(ws), ws_bytes / 8, static_cast<cudaStream_t>(stream)));
   return NB_OK;
 }
 
@@ -486,6 +486,15 @@ int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i) {
   if (precision_bytes == 8) return step_workspace_bytes<double>(n_i);
   fail(NB_ERR_ARG, "precision_bytes must be 4 or 8");
   return -1;
+}
+
+int64_t nb_energy_workspace_bytes(int precision_bytes, int64_t n) {
+  if (n < 1) n = 1;
+  if (precision_bytes != 4 && precision_bytes != 8) {
+    fail(NB_ERR_ARG, "precision_bytes must be 4 or 8");
+    return -1;
+  }
+  return 8 * energy_workspace_entries(precision_bytes, n);
 }
 
 int nb_dev_step_f32(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin, int64_t j_count,

@@ -2,6 +2,9 @@
 // updates, SoA/AoS <-> packed conversion at the boundary, and the FP64 energy
 // diagnostics.  All are HBM-bound and negligible next to the O(N^2) pass.
 #include "nbody_common.cuh"
+
+#include <algorithm>
+#include <cstdint>
 #include "nbody_kernels.h"
 
 namespace nb {
@@ -84,58 +87,119 @@ __global__ void unpack_aos_kernel(const V4<R>* in, R* xyz, int64_t n) {
   }
 }
 
-// Potential per body, phi_i = sum_{j != i} m_j / sqrt(|p_j - p_i|^2 + eps2), FP64.
+// Potential per body, phi_i = sum_{j != i} m_j / sqrt(|p_j - p_i|^2 + eps2), FP64
+// (validation.py:134-145 sums m_i m_j / r over i < j; -G/2 sum_i m_i phi_i is the
+// same energy).  Same structure as the FP64 force kernel: 256 threads x PK target
+// bodies, 256-body double4 source tiles in shared memory, MUFU.RSQ64H seed y0
+// with e = 1 - d2 y0^2 refined to m d2^(-1/2) = m y0 (1 + e/2 + 3e^2/8) -- 13 DP
+// ops per pair, no IEEE rsqrt slow path.  blockIdx.y splits the sources into
+// gridDim.y ranges (the grid fills the GPU at any N); phi[y*n + i] holds range
+// y's partial and energy_reduce_kernel adds the ranges in order (deterministic).
+constexpr int PK = 4;
 template <typename R>
-__global__ void __launch_bounds__(256) potential_kernel(const V4<R>* pos, int64_t n, double eps2, double* phi) {
+__global__ void __launch_bounds__(256) potential_kernel(const V4<R>* pos, int64_t n, double eps2, int64_t span,
+                                                       double* phi) {
   __shared__ double4 tile[256];
-  const int64_t i = blockIdx.x * 256LL + threadIdx.x;
-  const V4<R> pi = pos[i < n ? i : n - 1];
-  const double xi = pi.x, yi = pi.y, zi = pi.z;
-  double s = 0.0;
-  for (int64_t j0 = 0; j0 < n; j0 += 256) {
-    const int64_t j = j0 + threadIdx.x;
-    if (j < n) {
-      const V4<R> pj = pos[j];
-      tile[threadIdx.x] = make_double4(pj.x, pj.y, pj.z, pj.w);
+  const int tid = threadIdx.x;
+  const int64_t i0 = blockIdx.x * (256LL * PK) + tid;
+  const int64_t jlo = blockIdx.y * span, jhi = min(n, jlo + span);
+  double nx[PK], ny[PK], nz[PK], acc[PK];
+#pragma unroll
+  for (int k = 0; k < PK; ++k) {
+    const int64_t i = i0 + k * 256;
+    const V4<R> p = pos[i < n ? i : n - 1];
+    nx[k] = -(double)p.x; ny[k] = -(double)p.y; nz[k] = -(double)p.z;
+    acc[k] = 0.0;
+  }
+  for (int64_t j0 = jlo; j0 < jhi; j0 += 256) {
+    const int64_t j = j0 + tid;
+    if (j < jhi) {
+      const V4<R> q = pos[j];
+      tile[tid] = make_double4(q.x, q.y, q.z, q.w);
     }
     __syncthreads();
-    const int cnt = (int)(n - j0 < 256 ? n - j0 : 256);
+    const int cnt = (int)min((int64_t)256, jhi - j0);
+    int self[PK];  // tile index of target k itself, or -1
+#pragma unroll
+    for (int k = 0; k < PK; ++k) {
+      const int64_t rel = i0 + k * 256 - j0;
+      self[k] = (rel >= 0 && rel < cnt) ? (int)rel : -1;
+    }
+#pragma unroll 4
     for (int jj = 0; jj < cnt; ++jj) {
       const double4 q = tile[jj];
-      const double dx = q.x - xi, dy = q.y - yi, dz = q.z - zi;
-      const double t = q.w * rsqrt(dx * dx + dy * dy + dz * dz + eps2);
-      s += (j0 + jj == i) ? 0.0 : t;
+#pragma unroll
+      for (int k = 0; k < PK; ++k) {
+        const double dx = q.x + nx[k], dy = q.y + ny[k], dz = q.z + nz[k];
+        double d2 = fma(dx, dx, eps2);
+        d2 = fma(dy, dy, d2);
+        d2 = fma(dz, dz, d2);
+        const double y = rsqrt_seed(d2);
+        const double e = fma(-d2, y * y, 1.0);
+        const double my = q.w * y;
+        const double w = fma(my, e * fma(e, 0.375, 0.5), my);
+        acc[k] += (jj == self[k]) ? 0.0 : w;
+      }
     }
     __syncthreads();
   }
-  if (i < n) phi[i] = s;
+#pragma unroll
+  for (int k = 0; k < PK; ++k) {
+    const int64_t i = i0 + k * 256;
+    if (i < n) phi[blockIdx.y * n + i] = acc[k];
+  }
 }
 
-// Fixed-order block reduction: out6 = (KE, PE, Px, Py, Pz, KE+PE).
-template <typename R>
-__global__ void __launch_bounds__(1024) energy_reduce_kernel(const V4<R>* pos, const V4<R>* vel, const double* phi,
-                                                             int64_t n, double g, double* out6) {
-  __shared__ double red[5][1024];
-  double ke = 0, pe = 0, px = 0, py = 0, pz = 0;
-  for (int64_t i = threadIdx.x; i < n; i += 1024) {
-    const double m = pos[i].w;
-    const V4<R> v = vel[i];
-    const double vx = v.x, vy = v.y, vz = v.z;
-    ke += 0.5 * m * (vx * vx + vy * vy + vz * vz);
-    pe += m * phi[i];
-    px += m * vx; py += m * vy; pz += m * vz;
-  }
-  red[0][threadIdx.x] = ke; red[1][threadIdx.x] = pe;
-  red[2][threadIdx.x] = px; red[3][threadIdx.x] = py; red[4][threadIdx.x] = pz;
+// Fixed-order two-stage reduction: block b sums bodies [b*chunk, (b+1)*chunk)
+// (each body's potential over the source ranges in order) into part[b*5 + q],
+// q = (KE, m*phi, Px, Py, Pz); energy_final_kernel adds the blocks in order and
+// writes out6 = (KE, PE, Px, Py, Pz, KE+PE).  Deterministic at any grid.
+__device__ __forceinline__ void block_sum5(double v[5], double (*red)[256]) {
+#pragma unroll
+  for (int q = 0; q < 5; ++q) red[q][threadIdx.x] = v[q];
   __syncthreads();
-  for (int s = 512; s > 0; s >>= 1) {
+  for (int s = 128; s > 0; s >>= 1) {
     if (threadIdx.x < s)
-      for (int k = 0; k < 5; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + s];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + s];
     __syncthreads();
   }
+#pragma unroll
+  for (int q = 0; q < 5; ++q) v[q] = red[q][0];
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256) energy_partial_kernel(const V4<R>* pos, const V4<R>* vel, const double* phi,
+                                                             int64_t n, int ranges, int64_t chunk, double* part) {
+  __shared__ double red[5][256];
+  double v[5] = {0, 0, 0, 0, 0};
+  const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += 256) {
+    const double m = pos[i].w;
+    const V4<R> u = vel[i];
+    const double vx = u.x, vy = u.y, vz = u.z;
+    double ph = 0.0;
+    for (int r = 0; r < ranges; ++r) ph += phi[r * n + i];
+    v[0] += 0.5 * m * (vx * vx + vy * vy + vz * vz);
+    v[1] += m * ph;
+    v[2] += m * vx; v[3] += m * vy; v[4] += m * vz;
+  }
+  block_sum5(v, red);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) part[blockIdx.x * 5 + q] = v[q];
+}
+
+__global__ void __launch_bounds__(256) energy_final_kernel(const double* part, int blocks, double g, double* out6) {
+  __shared__ double red[5][256];
+  double v[5] = {0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < blocks; b += 256)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) v[q] += part[b * 5 + q];
+  block_sum5(v, red);
   if (threadIdx.x == 0) {
-    const double KE = red[0][0], PE = -0.5 * g * red[1][0];
-    out6[0] = KE; out6[1] = PE; out6[2] = red[2][0]; out6[3] = red[3][0]; out6[4] = red[4][0];
+    const double KE = v[0], PE = -0.5 * g * v[1];
+    out6[0] = KE; out6[1] = PE; out6[2] = v[2]; out6[3] = v[3]; out6[4] = v[4];
     out6[5] = KE + PE;
   }
 }
@@ -177,12 +241,57 @@ cudaError_t launch_unpack_aos(const V4<R>* in, R* xyz, int64_t n, cudaStream_t s
   count_launch();
   return cudaGetLastError();
 }
+// Plan of the diagnostics pass: source ranges of the potential kernel (the
+// fewest, each >= 1024 sources, that fill the resident CTA slots of the GPU to
+// >= 95 % -- or the best fill within the limit) and reduction blocks, within a
+// workspace of `entries` doubles (ranges*n potentials + 5 per reduction block).
+struct EnergyPlan {
+  int64_t ranges, blocks;
+};
+template <typename R>
+EnergyPlan energy_plan(int64_t n, int64_t entries) {
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, potential_kernel<R>, 256, 0);
+  const int64_t slots = (int64_t)sms * (occ < 1 ? 1 : occ);
+  const int64_t iblocks = (n + 256 * PK - 1) / (256 * PK);
+  EnergyPlan p{1, entries >= n + 5LL * sms ? (int64_t)sms : 1};
+  const int64_t rmax = std::min<int64_t>({std::max<int64_t>(1, n / 1024), 65535,
+                                          std::max<int64_t>(1, (entries - 5 * p.blocks) / n)});
+  double best = 0.0;
+  for (int64_t r = 1; r <= rmax; ++r) {
+    const int64_t ctas = iblocks * r;
+    const double fill = (double)ctas / (double)(((ctas + slots - 1) / slots) * slots);
+    if (fill > best + 1e-9) {
+      best = fill;
+      p.ranges = r;
+    }
+    if (fill >= 0.95) break;
+  }
+  return p;
+}
+
+int64_t energy_workspace_entries(int precision_bytes, int64_t n) {
+  const int64_t big = INT64_MAX / 16;
+  const EnergyPlan p = precision_bytes == 4 ? energy_plan<float>(n, big) : energy_plan<double>(n, big);
+  return p.ranges * n + 5 * p.blocks;
+}
+
 template <typename R>
 cudaError_t launch_energy(const V4<R>* pos, const V4<R>* vel, int64_t n, double g, double eps2, double* out6,
-                          double* phi, cudaStream_t s) {
-  potential_kernel<R><<<blocks_for(n, 256), 256, 0, s>>>(pos, n, eps2, phi);
-  energy_reduce_kernel<R><<<1, 1024, 0, s>>>(pos, vel, phi, n, g, out6);
-  count_launch(2);
+                          double* ws, int64_t ws_entries, cudaStream_t s) {
+  const EnergyPlan p = energy_plan<R>(n, ws_entries);
+  const int64_t iblocks = (n + 256 * PK - 1) / (256 * PK);
+  const int64_t span = ((n + p.ranges - 1) / p.ranges + 255) / 256 * 256;
+  const int64_t ranges = (n + span - 1) / span;
+  potential_kernel<R><<<dim3((unsigned)iblocks, (unsigned)ranges), 256, 0, s>>>(pos, n, eps2, span, ws);
+  // reduction partials after the potentials, or (no room) in out6 itself
+  double* part = p.blocks > 1 ? ws + ranges * n : out6;
+  const int64_t chunk = (n + p.blocks - 1) / p.blocks;
+  energy_partial_kernel<R><<<(unsigned)p.blocks, 256, 0, s>>>(pos, vel, ws, n, (int)ranges, chunk, part);
+  energy_final_kernel<<<1, 256, 0, s>>>(part, (int)p.blocks, g, out6);
+  count_launch(3);
   return cudaGetLastError();
 }
 
@@ -193,7 +302,7 @@ cudaError_t launch_energy(const V4<R>* pos, const V4<R>* vel, int64_t n, double 
   template cudaError_t launch_unpack_soa<R>(const V4<R>*, R*, R*, R*, int64_t, cudaStream_t);       \
   template cudaError_t launch_pack_aos<R>(const R*, const R*, V4<R>*, int64_t, cudaStream_t);       \
   template cudaError_t launch_unpack_aos<R>(const V4<R>*, R*, int64_t, cudaStream_t);               \
-  template cudaError_t launch_energy<R>(const V4<R>*, const V4<R>*, int64_t, double, double, double*, double*, cudaStream_t);
+  template cudaError_t launch_energy<R>(const V4<R>*, const V4<R>*, int64_t, double, double, double*, double*, int64_t, cudaStream_t);
 NB_INST(float)
 NB_INST(double)
 #undef NB_INST

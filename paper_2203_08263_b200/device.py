@@ -283,7 +283,7 @@ class DeviceState:
         if self.n_i != self.n:
             raise ValueError("energy diagnostics need the whole system on one device")
         out = torch.zeros(6, dtype=torch.float64, device=self.device)
-        ws = torch.empty(8 * self.n, dtype=torch.uint8, device=self.device)
+        ws = torch.empty(_native.energy_workspace_bytes(self.pbytes, self.n), dtype=torch.uint8, device=self.device)
         _native.call("nb_dev_energy" + self.sfx, self.pos_cur.data_ptr(), self.vel.data_ptr(), self.n,
                      g, eps2, out.data_ptr(), ws.data_ptr(), ws.numel(), self.stream_ptr())
         v = out.cpu().numpy()

@@ -650,14 +650,21 @@ def test_backend_simulate_matches_package():
     np.testing.assert_array_equal(np.stack(cols[:3], 1), nb.simulate(s, p).position_matrix())
 
 
-def test_energy_diagnostics(oracle):
-    s = cube(2048, 31, "double")
-    p = nb.SimParams(1.0, 1e-3, 1e-3, 1)
+@pytest.mark.parametrize("n,prec,eps2", [(2048, "double", 1e-3), (1, "double", 1e-3), (2, "double", 0.0),
+                                         (777, "single", 1e-2), (40000, "double", 1e-3), (65537, "single", 1e-4)])
+def test_energy_diagnostics(oracle, n, prec, eps2):
+    """nb_dev_energy (FP64 potential pass with source ranges + fixed-order
+    reduction) against the oracle's long-double diagnostics, ragged sizes, one
+    body, eps2 = 0 (self pair masked), FP32 systems upcast."""
+    s = cube(n, 31, prec)
+    p = nb.SimParams(1.0, 1e-3, eps2, 1)
     d = nb.diagnostics_gpu(s, p)
-    want = oracle.diagnostics(s.position_matrix(), np.stack(s.velocities, 1), s.masses, 1.0, 1e-3)
+    want = oracle.diagnostics(s.position_matrix(), np.stack(s.velocities, 1), s.masses, 1.0, eps2)
     assert abs(d["kinetic"] - want["kinetic"]) <= 1e-12 * abs(want["kinetic"])
-    assert abs(d["potential"] - want["potential"]) <= 1e-12 * abs(want["potential"])
-    np.testing.assert_allclose(d["momentum"], want["momentum"], rtol=1e-12, atol=1e-13)
+    assert abs(d["potential"] - want["potential"]) <= 1e-12 * max(abs(want["potential"]), 1e-300)
+    if n == 1:
+        assert d["potential"] == 0.0
+    np.testing.assert_allclose(d["momentum"], want["momentum"], rtol=1e-12, atol=1e-13 * n)
 
 
 @pytest.mark.parametrize("prec", ["double", "single"])
