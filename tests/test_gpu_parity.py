@@ -270,6 +270,30 @@ def test_momentum_conserved_from_rest():
     assert np.linalg.norm(m @ v) <= 1e-9 * float(np.sum(m * np.linalg.norm(v, axis=1)))
 
 
+def test_two_body_energy_drift():
+    """pkg/tests/test_acceptance.py:80-86 on the GPU path: unit two-body system,
+    dt = 1e-3, 100 steps, |E1 - E0| / |E0| <= 1e-4, energies from the GPU
+    diagnostics pass."""
+    params = nb.SimParams(1.0, 1e-3, 1e-9, 100)
+    e0 = nb.diagnostics_gpu(two_body(), params)["total"]
+    e1 = nb.diagnostics_gpu(nb.simulate(two_body(), params, nb.reference_variant()), params)["total"]
+    assert abs(e1 - e0) / abs(e0) <= 1e-4
+
+
+def test_second_order_convergence(oracle):
+    """pkg/tests/test_acceptance.py:88-100 on the GPU path: halving dt shrinks the
+    position error against a dt/2048 FP64 run (the oracle's simulate) by a factor
+    in [3, 5] -- velocity Verlet is second order."""
+    eps2, total = 0.25, 1.0
+    s = two_body()
+    fine, _ = oracle.simulate(s.position_matrix(), np.stack(s.velocities, 1), s.masses, 1.0, total / 2048, eps2,
+                              2048)
+    err = [float(np.max(np.abs(nb.simulate(two_body(), nb.SimParams(1.0, total / k, eps2, k),
+                                           nb.reference_variant()).position_matrix() - fine)))
+           for k in (128, 256)]
+    assert 3.0 <= err[0] / err[1] <= 5.0, err
+
+
 @pytest.mark.parametrize("prec,n", [("double", 20000), ("single", 20000), ("single", 70000)])
 def test_runs_are_bitwise_reproducible(prec, n):
     """Also covers the TMA-staged FP32 path (N >= 65536)."""
