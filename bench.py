@@ -209,15 +209,23 @@ def run_ours(args) -> dict:
     from paper_2203_08263_b200 import _native
     from paper_2203_08263_b200._native import NB_STEP_FINAL_KICK, NB_STEP_FIRST, NB_STEP_KICK_DRIFT
     from paper_2203_08263_b200.device import DeviceState, kernel_flags, needs_self_mask
-    from paper_2203_08263_b200.sharded import pad_system, run_sharded, shard_range
+    from paper_2203_08263_b200.sharded import gather_into, pad_system, run_sharded, shard_range
 
     world, rank, local = _dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # One process per GPU.  Test hook (never the measured configuration):
+    # NB_BENCH_BACKEND=gloo with more ranks than GPUs runs the multi-rank driver
+    # logic with ranks sharing a device and a host-side exchange.
+    local_dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
+    backend = os.environ.get("NB_BENCH_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = nb.BASELINE_CONFIGS[args.config]
     params = cfg.params()
     sys0 = cfg.system()
@@ -268,13 +276,16 @@ def run_ours(args) -> dict:
             return None
 
         def gather(full, local_rows):
-            return dist.all_gather_into_tensor(full, local_rows, async_op=True)
+            return gather_into(full, local_rows, async_op=True)
         run_sharded(state, g, dt, eps2, steps, mask, gather, world)
         return None
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local_dev])
+            else:
+                dist.barrier()
 
     # ---------------------------------------------------------------- warm-up
     for _ in range(args.warmup):
@@ -283,7 +294,7 @@ def run_ours(args) -> dict:
     torch.cuda.synchronize()
 
     # ---------------------------------------------------------------- timed region
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local_dev)
     clocks.start()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -311,7 +322,7 @@ def run_ours(args) -> dict:
     clk = clocks.stop()
     total_s = sum(step_ms) / 1e3
     if world > 1:
-        t = torch.tensor([total_s], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_s], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_s = float(t.item())
     interactions = float(cfg.n) * cfg.n * (steps + 1) * args.steps
@@ -356,7 +367,7 @@ def run_ours(args) -> dict:
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         e2e = {"value": interactions / e2e_s, "unit": UNIT,

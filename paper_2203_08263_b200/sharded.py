@@ -111,11 +111,31 @@ def run_sharded_p2p(state, g: float, dt: float, eps2: float, steps: int, flags: 
     barrier()
 
 
-def _torch_allgather(group):
+class _Done:
+    """Handle of an exchange that already completed (host-staged path)."""
+
+    def wait(self) -> None:
+        return None
+
+
+def gather_into(full, local, group=None, async_op: bool = False):
+    """In-place all-gather of this rank's rows ``local`` (a slice of ``full``)
+    into ``full`` on every rank.  NCCL: one in-place ncclAllGather on the device
+    buffers.  Any other backend (gloo, for CPU-side tests of the multi-rank
+    driver) is staged through host memory."""
     import torch.distributed as dist
 
+    if full.device.type != "cuda" or dist.get_backend(group) == "nccl":
+        return dist.all_gather_into_tensor(full, local, group=group, async_op=async_op)
+    host = full.cpu()
+    dist.all_gather_into_tensor(host, local.cpu(), group=group)
+    full.copy_(host)
+    return _Done() if async_op else None
+
+
+def _torch_allgather(group):
     def gather(full, local):
-        return dist.all_gather_into_tensor(full, local, group=group, async_op=True)
+        return gather_into(full, local, group, async_op=True)
     return gather
 
 
@@ -187,7 +207,7 @@ def simulate_sharded(positions: np.ndarray, velocities: np.ndarray, masses: np.n
     else:
         raise ValueError(f"unknown transport {transport!r} (expected 'nccl' or 'p2p')")
     vel_full = torch.empty((npad, 4), dtype=state.vel.dtype, device=state.device)
-    dist.all_gather_into_tensor(vel_full, state.vel[:ni].contiguous(), group=group)
+    gather_into(vel_full, state.vel[:ni].contiguous(), group)
     out_pos = state.pos_cur[:n, :3].cpu().numpy()
     out_vel = vel_full[:n, :3].cpu().numpy()
     return out_pos, out_vel
