@@ -173,6 +173,26 @@ def _p2p_setup(pos, vel, m, dtype, i0, ni, group):
     return state, peer_next, barrier
 
 
+_SHARD_CACHE: dict = {}
+
+
+def _shard_state(pos, vel, m, dtype, i0: int, ni: int):
+    """The rank's DeviceState, reused across simulate_sharded calls with the same
+    shape (device buffers and pinned staging are allocated once; load() refills)."""
+    import torch
+
+    from .device import DeviceState
+    key = (pos.shape[0], np.dtype(dtype).str, i0, ni, torch.cuda.current_device())
+    st = _SHARD_CACHE.get(key)
+    if st is None:
+        if len(_SHARD_CACHE) >= 4:
+            _SHARD_CACHE.clear()
+        st = _SHARD_CACHE[key] = DeviceState(pos, vel, m, dtype, i_begin=i0, n_i=ni)
+    else:
+        st.load(pos, vel, m)
+    return st
+
+
 def simulate_sharded(positions: np.ndarray, velocities: np.ndarray, masses: np.ndarray, dtype,
                      g: float, dt: float, eps2: float, steps: int, group=None,
                      flags: Optional[int] = None, transport: str = "nccl") -> Tuple[np.ndarray, np.ndarray]:
@@ -202,7 +222,7 @@ def simulate_sharded(positions: np.ndarray, velocities: np.ndarray, masses: np.n
         state, peer_next, barrier = _p2p_setup(pos, vel, m, dtype, i0, ni, group)
         run_sharded_p2p(state, g, dt, eps2, steps, flags, peer_next, barrier)
     elif transport == "nccl":
-        state = DeviceState(pos, vel, m, dtype, i_begin=i0, n_i=ni)
+        state = _shard_state(pos, vel, m, dtype, i0, ni)
         run_sharded(state, g, dt, eps2, steps, flags, _torch_allgather(group), world)
     else:
         raise ValueError(f"unknown transport {transport!r} (expected 'nccl' or 'p2p')")
