@@ -604,6 +604,14 @@ int nb_dev_init_f64(int kind, uint64_t seed, int64_t n, void* pos4, void* vel4, 
 }
 
 const char* nb_last_error(void) { return t_err.c_str(); }
+
+#if NB_TRACE
+// Trace builds only (tools/trace_launches.py): per-CTA timeline records.
+__attribute__((visibility("default"))) int nb_trace_setup(void* buf, int64_t capacity) {
+  return nb::trace_setup(buf, capacity);
+}
+__attribute__((visibility("default"))) int64_t nb_trace_count(void) { return nb::trace_count(); }
+#endif
 const char* nb_version(void) { return "nbody_b200 0.1.0 (sm_100a)"; }
 int64_t nb_launch_count(void) { return g_launches.load(); }
 

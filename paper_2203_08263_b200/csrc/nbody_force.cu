@@ -73,6 +73,12 @@
 #ifndef NB_CHUNK
 #define NB_CHUNK 16
 #endif
+#ifndef NB_FIXUP_THREADS
+// Threads per fixup CTA (one split body each).  Small CTAs spread the
+// latency-bound fixup over every SM: C2 +1.7 % against 256-thread CTAs
+// (profiles/variants_r01_fixup_threads.txt).
+#define NB_FIXUP_THREADS 32
+#endif
 #ifndef NB_F64_K
 #define NB_F64_K 6
 #endif
@@ -101,6 +107,39 @@ namespace nb {
 #define NB_DCHECK(cond) do { if (!(cond)) __trap(); } while (0)
 #else
 #define NB_DCHECK(cond) do { } while (0)
+#endif
+
+#if NB_TRACE
+// Timeline instrumentation (trace builds only, tools/trace_launches.py): thread 0
+// of every CTA records (tag, cta, smid, t_entry, t_wait, t_end) in %globaltimer ns.
+__device__ unsigned long long* g_trace = nullptr;
+__device__ unsigned long long g_trace_n = 0;
+__device__ unsigned long long g_trace_cap = 0;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_rec(int tag, unsigned long long t_entry, unsigned long long t_wait) {
+  __syncthreads();
+  if (threadIdx.x == 0 && g_trace) {
+    const unsigned long long t_end = gtimer();
+    const unsigned long long k = atomicAdd(&g_trace_n, 1ull);
+    if (k < g_trace_cap) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      unsigned long long* r = g_trace + 6 * k;
+      r[0] = tag; r[1] = blockIdx.x; r[2] = smid; r[3] = t_entry; r[4] = t_wait; r[5] = t_end;
+    }
+  }
+}
+#define NB_TRACE_ENTRY() const unsigned long long nb_t_entry = gtimer()
+#define NB_TRACE_WAITED() const unsigned long long nb_t_wait = gtimer()
+#define NB_TRACE_END(tag) trace_rec(tag, nb_t_entry, nb_t_wait)
+#else
+#define NB_TRACE_ENTRY() do { } while (0)
+#define NB_TRACE_WAITED() do { } while (0)
+#define NB_TRACE_END(tag) do { } while (0)
 #endif
 
 struct Sched {
@@ -697,9 +736,12 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
   }
   // Programmatic dependent launch: wait for the previous kernel in the stream
   // (positions it wrote), then let the fixup kernel be scheduled as our CTAs drain.
+  NB_TRACE_ENTRY();
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  NB_TRACE_WAITED();
   asm volatile("griddepcontrol.launch_dependents;");
   step_body<Core, T, TJ, CH, false, TMA>(a, tile, s_sums, mbar);
+  NB_TRACE_END(1);
 }
 
 // ---------------------------------------------------------------- split i-block fixup
@@ -711,11 +753,14 @@ __device__ __forceinline__ void fixup_body(const StepArgs<R>& a, int64_t il);
 // segment, 2c+1 its last) and run the epilogue.  Bodies of i-blocks one CTA
 // covered whole were finished by step_kernel and are skipped.
 template <typename R, int IB>
-__global__ void __launch_bounds__(256) fixup_kernel(const StepArgs<R> a) {
+__global__ void __launch_bounds__(NB_FIXUP_THREADS) fixup_kernel(const StepArgs<R> a) {
+  NB_TRACE_ENTRY();
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  NB_TRACE_WAITED();
   asm volatile("griddepcontrol.launch_dependents;");
-  const int64_t il = blockIdx.x * 256LL + threadIdx.x;
+  const int64_t il = blockIdx.x * (int64_t)NB_FIXUP_THREADS + threadIdx.x;
   fixup_body<R, IB>(a, il);
+  NB_TRACE_END(2);
   if (a.n_peers) __threadfence_system();  // peer stores visible before the rank barrier
 }
 
@@ -912,8 +957,8 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   for (int64_t b = 0; b < g.n_iblocks && !split; ++b)
     split = host_cta_of(b * g.n_tiles, grid, g.units) != host_cta_of(b * g.n_tiles + g.n_tiles - 1, grid, g.units);
   if (split) {
-    cfg.gridDim = dim3((unsigned)((a.n_i + 255) / 256));
-    cfg.blockDim = dim3(256);
+    cfg.gridDim = dim3((unsigned)((a.n_i + NB_FIXUP_THREADS - 1) / NB_FIXUP_THREADS));
+    cfg.blockDim = dim3(NB_FIXUP_THREADS);
     e = cudaLaunchKernelEx(&cfg, fixup_kernel<R, IB>, a);
     count_launch();
   }
@@ -956,6 +1001,22 @@ cudaError_t launch_simulate_persistent(StepArgs<R> a, int flags, V4<R>* pos_a, V
   count_launch();
   return e;
 }
+
+#if NB_TRACE
+int trace_setup(void* buf, int64_t cap) {
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  unsigned long long c = (unsigned long long)cap, z = 0;
+  if (cudaMemcpyToSymbol(g_trace, &p, sizeof(p)) != cudaSuccess) return 1;
+  if (cudaMemcpyToSymbol(g_trace_cap, &c, sizeof(c)) != cudaSuccess) return 1;
+  if (cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z)) != cudaSuccess) return 1;
+  return 0;
+}
+int64_t trace_count() {
+  unsigned long long n = 0;
+  cudaMemcpyFromSymbol(&n, g_trace_n, sizeof(n));
+  return (int64_t)n;
+}
+#endif
 
 template <typename R>
 int64_t step_workspace_bytes(int64_t n_i) {

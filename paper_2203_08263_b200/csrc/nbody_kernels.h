@@ -64,7 +64,11 @@ template <typename R> cudaError_t launch_unpack_aos(const V4<R>* in, R* xyz, int
 // kind 0: uniform cube, 1: Plummer sphere (BASELINE.json generators).
 template <typename R> cudaError_t launch_init(int kind, unsigned long long seed, int64_t n, V4<R>* pos, V4<R>* vel,
                                               cudaStream_t s);
-int64_t energy_workspace_entries(int precision_bytes, int64_t n);  // doubles of workspace the energy pass can use
+int64_t energy_workspace_entries(int precision_bytes, int64_t n);
+#if NB_TRACE
+int trace_setup(void* buf, int64_t cap);
+int64_t trace_count();
+#endif  // doubles of workspace the energy pass can use
 template <typename R> cudaError_t launch_energy(const V4<R>* pos, const V4<R>* vel, int64_t n, double g, double eps2,
                                                double* out6, double* phi, int64_t phi_entries, cudaStream_t s);
 
