@@ -24,6 +24,7 @@ m*d*rsqrt(d2)^3, which the reference pins as equivalent to both forms
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, replace
 from enum import Enum
 from typing import Optional, Tuple
@@ -200,9 +201,10 @@ def compute_accelerations(sys_, params, variant: Optional[KernelVariant] = None,
     m = np.asarray(sys_.masses, dtype)
     eps2 = params.softening_sq
     z = np.zeros(pos.shape[0], dtype)
-    st = _resident_state((pos[:, 0], pos[:, 1], pos[:, 2]), (z, z, z), m, dtype)
-    a = st.accelerations(params.gravitational_constant, eps2, kernel_flags(m, eps2, dtype))
-    host = a[:, :3].cpu().numpy()
+    with _STATE_LOCK:
+        st = _resident_state((pos[:, 0], pos[:, 1], pos[:, 2]), (z, z, z), m, dtype)
+        a = st.accelerations(params.gravitational_constant, eps2, kernel_flags(m, eps2, dtype))
+        host = a[:, :3].cpu().numpy()
     out.x[...] = host[:, 0]
     out.y[...] = host[:, 1]
     out.z[...] = host[:, 2]
@@ -255,12 +257,17 @@ def simulate_arrays(positions, velocities, masses, softening_sq: float, dt: floa
     if _distributed_world(group) > 1:
         from .sharded import simulate_sharded
         return simulate_sharded(pos, vel, m, dtype, G, dt, softening_sq, steps, group=group)
-    st = _resident_state((pos[:, 0], pos[:, 1], pos[:, 2]), (vel[:, 0], vel[:, 1], vel[:, 2]), m, dtype)
-    st.simulate(G, dt, softening_sq, steps, kernel_flags(m, softening_sq, dtype))
-    return st.positions_host(), st.velocities_host()
+    with _STATE_LOCK:
+        st = _resident_state((pos[:, 0], pos[:, 1], pos[:, 2]), (vel[:, 0], vel[:, 1], vel[:, 2]), m, dtype)
+        st.simulate(G, dt, softening_sq, steps, kernel_flags(m, softening_sq, dtype))
+        pc, vc = st.columns_host()
+    return np.stack(pc, 1), np.stack(vc, 1)
 
 
 _STATE_CACHE: dict = {}
+# Calls share cached device states: one caller at a time (the reference's
+# harness is single-threaded too, harness.py:5-6).
+_STATE_LOCK = threading.RLock()
 
 
 def _resident_state(pos, vel, m, dtype):
@@ -302,10 +309,11 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
     # back unpacked on the device in one D2H.
     from .device import kernel_flags
     m = np.asarray(sys_.masses, dtype)
-    st = _resident_state(_columns(sys_, "positions"), _columns(sys_, "velocities"), m, dtype)
-    st.simulate(params.gravitational_constant, params.dt, params.softening_sq, params.steps,
-                kernel_flags(m, params.softening_sq, dtype))
-    pos, vel = st.columns_host()
+    with _STATE_LOCK:
+        st = _resident_state(_columns(sys_, "positions"), _columns(sys_, "velocities"), m, dtype)
+        st.simulate(params.gravitational_constant, params.dt, params.softening_sq, params.steps,
+                    kernel_flags(m, params.softening_sq, dtype))
+        pos, vel = st.columns_host()
     if _value(sys_.layout) != "soa":
         pos, vel = np.stack(pos, 1), np.stack(vel, 1)
     return type(sys_)(sys_.layout, sys_.precision, pos, vel, sys_.masses.copy())
