@@ -120,18 +120,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ void trace_rec(int tag, unsigned long long t_entry, unsigned long long t_wait) {
-  __syncthreads();
+// Record: (tag, id, smid, t[0..4]); unused timestamps are 0.
+__device__ __forceinline__ void trace_put(int tag, unsigned long long id, const unsigned long long* t, int nt) {
   if (threadIdx.x == 0 && g_trace) {
-    const unsigned long long t_end = gtimer();
     const unsigned long long k = atomicAdd(&g_trace_n, 1ull);
     if (k < g_trace_cap) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      unsigned long long* r = g_trace + 6 * k;
-      r[0] = tag; r[1] = blockIdx.x; r[2] = smid; r[3] = t_entry; r[4] = t_wait; r[5] = t_end;
+      unsigned long long* r = g_trace + 8 * k;
+      r[0] = tag; r[1] = id; r[2] = smid;
+      for (int q = 0; q < 5; ++q) r[3 + q] = q < nt ? t[q] : 0ull;
     }
   }
+}
+__device__ __forceinline__ void trace_rec(int tag, unsigned long long t_entry, unsigned long long t_wait) {
+  __syncthreads();
+  const unsigned long long t[3] = {t_entry, t_wait, gtimer()};
+  trace_put(tag, blockIdx.x, t, 3);
 }
 #define NB_TRACE_ENTRY() const unsigned long long nb_t_entry = gtimer()
 #define NB_TRACE_WAITED() const unsigned long long nb_t_wait = gtimer()
@@ -804,22 +809,42 @@ __global__ void __launch_bounds__(T, MINB) simulate_kernel(StepArgs<typename Cor
   __shared__ double s_sums[Core::SMEM_SUMS * T];
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   for (int64_t s = 0; s <= steps; ++s) {
+#if NB_TRACE
+    unsigned long long tt[5];
+    tt[0] = gtimer();
+#endif
     a.mode = s == 0 ? NB_STEP_MODE_FIRST : (s < steps ? NB_STEP_MODE_KICK_DRIFT : NB_STEP_MODE_FINAL);
     a.pos = (s & 1) ? pos_b : pos_a;
     a.pos_next = (s & 1) ? pos_a : pos_b;
     step_body<Core, T, TJ, CH, true, false>(a, tile, s_sums, nullptr);
+#if NB_TRACE
+    __syncthreads();
+    tt[1] = gtimer();
+    tt[2] = tt[3] = tt[1];
+#endif
     if (any_split) {
       grid.sync();  // every partial slot of this step is written
+#if NB_TRACE
+      tt[2] = gtimer();
+#endif
       for (int64_t il = blockIdx.x * (int64_t)T + threadIdx.x; il < a.n_i; il += (int64_t)gridDim.x * T)
         fixup_body<R, IB>(a, il);
+#if NB_TRACE
+      __syncthreads();
+      tt[3] = gtimer();
+#endif
     }
     grid.sync();  // all new positions/velocities visible; nobody still reads the old buffer
+#if NB_TRACE
+    tt[4] = gtimer();
+    trace_put(3, (unsigned long long)blockIdx.x | ((unsigned long long)s << 32), tt, 5);
+#endif
   }
 }
 
 // ---------------------------------------------------------------- configurations
-// FP32: 128 threads x 6 bodies (3 FFMA2 pairs) = 768-body i-blocks, 256-body tiles.
-// FP64: 128 threads x 4 bodies = 512-body i-blocks, 128-body tiles.
+// Both precisions: 256 threads x 6 target bodies = 1536-body i-blocks, 256-body
+// source tiles (FP32: 3 packed FFMA2 pairs per thread).
 template <bool M, bool U> struct CoreF32M : CoreF32<NB_F32_K, M, NB_F32_UNROLL, U> {
   static constexpr bool MASK_SELF = M;
 };

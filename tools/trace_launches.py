@@ -30,7 +30,7 @@ fn.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_double, ctypes.c
                                        ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]
 flag = ctypes.c_int(0)
 cap = 1 << 20
-buf = torch.zeros(6 * cap, dtype=torch.int64, device="cuda")
+buf = torch.zeros(8 * cap, dtype=torch.int64, device="cuda")
 L.nb_trace_setup.argtypes = [ctypes.c_void_p, ctypes.c_int64]
 L.nb_trace_count.restype = ctypes.c_int64
 
@@ -46,7 +46,22 @@ assert L.nb_trace_setup(buf.data_ptr(), cap) == 0
 sim()
 torch.cuda.synchronize()
 n = L.nb_trace_count()
-r = buf[: 6 * min(n, cap)].view(-1, 6).cpu().numpy()
+r = buf[: 8 * min(n, cap)].view(-1, 8).cpu().numpy()
+if (r[:, 0] == 3).any():  # persistent simulate_kernel: per CTA per step (start, pass, sync1, fixup, sync2)
+    p = r[r[:, 0] == 3]
+    step = p[:, 1] >> 32
+    base = p[:, 3].min()
+    print(f"# {name}: persistent kernel, {len(p)} (CTA, step) records; per step, us (median over CTAs)\n")
+    print("| step | pass | wait at sync 1 | fixup | wait at sync 2 | step total |")
+    print("|---|---|---|---|---|---|")
+    for k in np.unique(step):
+        q = p[step == k]
+        t0, t1, t2, t3, t4 = (q[:, 3 + i].astype(np.float64) for i in range(5))
+        print(f"| {k} | {np.median(t1 - t0) / 1e3:.2f} | {np.median(t2 - t1) / 1e3:.2f} | {np.median(t3 - t2) / 1e3:.2f} | "
+              f"{np.median(t4 - t3) / 1e3:.2f} | {np.median(t4 - t0) / 1e3:.2f} |")
+    print(f"\nmax pass {np.max(p[:, 4] - p[:, 3]) / 1e3:.2f} us, max fixup {np.max(p[:, 6] - p[:, 5]) / 1e3:.2f} us")
+    sys.exit(0)
+r = r[:, :6]
 t0 = r[:, 3].min()
 r[:, 3:] -= t0
 # launches: consecutive groups in time order of (tag, wait time)

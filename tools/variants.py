@@ -15,12 +15,6 @@ OUT = os.path.join(HERE, "variants")
 VARIANTS = {
     "base": {},
     "trace": {"NB_TRACE": 1},
-    "trace_ft64": {"NB_TRACE": 1, "NB_FIXUP_THREADS": 64},
-    "trace_ft128": {"NB_TRACE": 1, "NB_FIXUP_THREADS": 128},
-    "trace_ft32": {"NB_TRACE": 1, "NB_FIXUP_THREADS": 32},
-    "ft64": {"NB_FIXUP_THREADS": 64},
-    "ft128": {"NB_FIXUP_THREADS": 128},
-    "ft32": {"NB_FIXUP_THREADS": 32},
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
