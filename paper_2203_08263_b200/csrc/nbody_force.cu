@@ -63,9 +63,13 @@
 #define NB_F32_STAGEWISE 0
 #endif
 #ifndef NB_F32_EXP2_MASK
-// Which (target pair q, source parity p) weights go through MUFU.LG2/EX2 instead
-// of MUFU.RSQ + FMUL2s: bit q + (K/2)*p.  0 = none.
-#define NB_F32_EXP2_MASK 17  // pair 0 on even sources, pair 1 on odd: 1/3 of the weights (measured best)
+// Which (target pair q, source phase p = jj mod NB_F32_EXP2_PHASES) weights go
+// through MUFU.LG2/EX2 instead of MUFU.RSQ + FMUL2s: bit q + (K/2)*p.  0 = none.
+// Default: pair 0 on even sources, pair 1 on odd -- 1/3 of the weights.
+#define NB_F32_EXP2_MASK 17
+#endif
+#ifndef NB_F32_EXP2_PHASES
+#define NB_F32_EXP2_PHASES 2
 #endif
 #ifndef NB_TMA_MIN_N
 #define NB_TMA_MIN_N 65536  // FP32 launches with >= this many targets and sources use TMA staging
@@ -228,7 +232,7 @@ struct CoreF32 {
   using R = float;
   static constexpr int K = K_;
   static constexpr int KP = K / 2;
-  static constexpr unsigned XMASK = NB_F32_EXP2_MASK & ((1u << (2 * KP)) - 1u);  // LG2/EX2 weights
+  static constexpr unsigned XMASK = NB_F32_EXP2_MASK & ((1u << (NB_F32_EXP2_PHASES * KP)) - 1u);  // LG2/EX2 weights
   static constexpr bool NEEDS_LM = XMASK != 0 && !UNI;  // needs log2(m_j) per source
   const float* lmt;  // this tile's log2(m_j) (NEEDS_LM)
 #if NB_F32_SUMS_IN_REGS
@@ -285,7 +289,7 @@ struct CoreF32 {
     upk(d2, d2a, d2b);
     f2x w;
 #if NB_F32_MATH == 0
-    if ((XMASK >> (q + KP * (jj & 1))) & 1u) {
+    if ((XMASK >> (q + KP * (jj % NB_F32_EXP2_PHASES))) & 1u) {
       // m d2^(-3/2) = 2^(-1.5 log2 d2 + log2 m): one FFMA2 and four MUFU ops in
       // place of three FMUL2 + two MUFU.RSQ -- moves FP32-pipe work onto the XU
       // pipe, which the rsqrt form leaves ~40 % idle.
