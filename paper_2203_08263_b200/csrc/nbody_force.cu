@@ -601,6 +601,10 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
     const int64_t t1 = min(NT, t0 + (u_end - u));
     // this segment's source offsets [s0, s1) within the j range
     const int64_t s0 = t0 * CH, s1 = min(t1 * CH, a.j_count);
+#if NB_TRACE
+    unsigned long long tseg[5];
+    tseg[0] = gtimer();
+#endif
 
 #pragma unroll
     for (int q = 0; q < K / 2; ++q) {
@@ -654,6 +658,9 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
       store_tile(0);
       __syncthreads();
     }
+#if NB_TRACE
+    tseg[1] = gtimer();
+#endif
 
     int buf = 0;
     for (int64_t lo = s0; lo < s1; lo += TJ) {
@@ -704,6 +711,9 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
       __syncthreads();
     }
 
+#if NB_TRACE
+    tseg[2] = gtimer();
+#endif
     if (t0 == 0 && t1 == NT) {
       // The whole source range of this i-block was ours: finish directly.
 #pragma unroll
@@ -725,6 +735,12 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
         sp[2 * IB + k * T + tid] = core.sum(2, k);
       }
     }
+#if NB_TRACE
+    __syncthreads();
+    tseg[3] = gtimer();
+    tseg[4] = (unsigned long long)(s1 - s0);
+    trace_put(4, (unsigned long long)c | ((unsigned long long)(u - u_begin) << 32), tseg, 5);
+#endif
     u += t1 - t0;
   }
   if (a.n_peers) __threadfence_system();  // peer stores visible before the rank barrier

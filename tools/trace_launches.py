@@ -61,6 +61,17 @@ if (r[:, 0] == 3).any():  # persistent simulate_kernel: per CTA per step (start,
               f"{np.median(t4 - t3) / 1e3:.2f} | {np.median(t4 - t0) / 1e3:.2f} |")
     print(f"\nmax pass {np.max(p[:, 4] - p[:, 3]) / 1e3:.2f} us, max fixup {np.max(p[:, 6] - p[:, 5]) / 1e3:.2f} us")
     sys.exit(0)
+seg = r[r[:, 0] == 4]
+if len(seg):  # per stream-K segment: start, first tile staged, tiles done, epilogue done, #sources
+    setup = (seg[:, 4] - seg[:, 3]) / 1e3
+    loop = (seg[:, 5] - seg[:, 4]) / 1e3
+    epi = (seg[:, 6] - seg[:, 5]) / 1e3
+    nsrc = seg[:, 7]
+    per_src = loop / np.maximum(nsrc, 1) * 1e3
+    print(f"# segments: {len(seg)}; median setup (targets + first tile) {np.median(setup):.2f} us, "
+          f"loop {np.median(loop):.2f} us for {np.median(nsrc):.0f} sources ({np.median(per_src):.2f} ns/source), "
+          f"epilogue {np.median(epi):.2f} us; per CTA per launch: segments {len(seg) / max(1, len(np.unique(seg[:, 1] & 0xffffffff))):.2f}\n")
+r = r[r[:, 0] != 4]
 r = r[:, :6]
 t0 = r[:, 3].min()
 r[:, 3:] -= t0

@@ -14,10 +14,7 @@ OUT = os.path.join(HERE, "variants")
 
 VARIANTS = {
     "base": {},
-    "p4_m1105": {"NB_F32_EXP2_PHASES": 4, "NB_F32_EXP2_MASK": 1105},   # = base pattern (1/3)
-    "p4_f5_1123": {"NB_F32_EXP2_PHASES": 4, "NB_F32_EXP2_MASK": 1123},  # 5/12
-    "p4_f3_1057": {"NB_F32_EXP2_PHASES": 4, "NB_F32_EXP2_MASK": 1057},  # 3/12: q0 p0, q2 p1, q1 p3
-    "p4_f5b_1361": {"NB_F32_EXP2_PHASES": 4, "NB_F32_EXP2_MASK": 1361},  # 5/12 alt
+    "trace": {"NB_TRACE": 1},  # per-CTA timelines for tools/trace_launches.py
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
