@@ -270,6 +270,57 @@ def test_momentum_conserved_from_rest():
     assert np.linalg.norm(m @ v) <= 1e-9 * float(np.sum(m * np.linalg.norm(v, axis=1)))
 
 
+def test_integrate_direct_substitution():
+    """pkg/tests/test_kernels.py:118-124: dv = a*dt, dp = (v_old + dv/2)*dt, exact."""
+    s = nb.system_from_arrays([[0.0, 0.0, 0.0]], np.zeros((1, 3)), [1.0])
+    acc = nb.AccelerationBuffer.allocate(1, nb.Precision.DOUBLE)
+    acc.x[0] = 1.0
+    nb.integrate_step(s, acc, nb.SimParams(1.0, 1.0, 1e-9, 1), nb.reference_variant())
+    assert s.velocities[0][0] == 1.0
+    assert s.positions[0][0] == 0.5
+
+
+def test_integrate_two_body_first_step():
+    """pkg/tests/test_kernels.py:127-140: the first kick-drift of the unit
+    two-body system, expected values as the update rule evaluates them."""
+    s = two_body()
+    params = nb.SimParams(1.0, 0.1, 0.0, 1)
+    acc = accel_of(s, params)
+    nb.integrate_step(s, acc, params, nb.reference_variant())
+    assert s.velocities[0][0] == 0.1 and s.velocities[0][1] == -0.1
+    assert s.positions[0][0] == (0.0 + 0.5 * 0.1) * 0.1
+    assert s.positions[0][1] == 1.0 + (0.0 + 0.5 * -0.1) * 0.1
+
+
+LADDER_SUBSET = [
+    nb.KernelVariant(nb.Layout.SOA, nb.MathForm.RECIPROCAL_MULTIPLY),
+    nb.KernelVariant(nb.Layout.SOA, block=8),
+    nb.KernelVariant(nb.Layout.SOA, block=64),
+    nb.KernelVariant(nb.Layout.SOA, block=128),
+    nb.KernelVariant(nb.Layout.SOA, nb.MathForm.RECIPROCAL_MULTIPLY, 32, 2),
+    nb.KernelVariant(nb.Layout.SOA, threads=4),
+    nb.KernelVariant(nb.Layout.AOS),
+]
+
+
+@pytest.mark.parametrize("variant", LADDER_SUBSET, ids=lambda v: f"{v.name}-T{v.threads}")
+def test_variant_equivalence_small(variant, oracle):
+    """pkg/tests/test_kernels.py:190-201 and :212-217 on the GPU path: every
+    ladder rung reproduces the FP64 reference checksum (the oracle's simulate of
+    the same state) within 1e-9 in FP64 and 5e-4 in FP32."""
+    params = nb.SimParams(1.0, 0.01, 1e-9, 10)
+    s64 = nb.init_system(192, nb.Seed(42))
+    fin, _ = oracle.simulate(s64.position_matrix(), np.stack(s64.velocities, 1), s64.masses, 1.0, 0.01, 1e-9, 10,
+                             recip=False)
+    ref = oracle.checksum(fin)
+    got = nb.checksum(nb.simulate(nb.init_system(192, nb.Seed(42), nb.Precision.DOUBLE, variant.layout),
+                                  params, variant))
+    assert abs(got - ref) / abs(ref) <= 1e-9
+    got32 = nb.checksum(nb.simulate(nb.init_system(192, nb.Seed(42), nb.Precision.SINGLE, variant.layout),
+                                    params, variant))
+    assert abs(got32 - ref) / abs(ref) <= 5e-4
+
+
 def test_two_body_energy_drift():
     """pkg/tests/test_acceptance.py:80-86 on the GPU path: unit two-body system,
     dt = 1e-3, 100 steps, |E1 - E0| / |E0| <= 1e-4, energies from the GPU
