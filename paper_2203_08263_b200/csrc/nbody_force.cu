@@ -10,7 +10,9 @@
 //    (3 FADD, 3 FFMA for d2, 3 FMUL for m*r^3, 3 FFMA accumulate) and one
 //    MUFU.RSQ.  Two target bodies are paired in each thread and every FP32 op is
 //    the packed FFMA2/FADD2/FMUL2 form with the source body broadcast (.F32
-//    operand), so the FP32 pipe -- not the issue slot -- is the bound.
+//    operand), so the FP32 pipe -- not the issue slot -- is the bound.  A third
+//    of the weights take m*2^(-1.5 log2 d2) through MUFU.LG2/EX2 instead (10
+//    FP32 ops + 2 MUFU), balancing the FMA and XU pipes (NB_F32_EXP2_MASK).
 //  * Source bodies are staged through shared memory in tiles of TJ packed
 //    (x,y,z,m) 4-vectors, double-buffered with one __syncthreads per tile; the
 //    inner loop reads them with broadcast LDS.128 (no bank conflicts: every lane
@@ -24,8 +26,9 @@
 //    space: a persistent grid of SMs x occupancy CTAs, each owning an equal
 //    contiguous range of units, so every SM gets the same work at every N.  An
 //    i-block split between CTAs is combined through FP64 partial slots by
-//    fixup_kernel (programmatic dependent launch) in fixed CTA order -- bitwise
-//    reproducible run to run -- which then runs the epilogue.
+//    fixup_kernel (programmatic dependent launch, 32-thread CTAs) in fixed CTA
+//    order -- bitwise reproducible run to run -- which then runs the epilogue.
+//  * NB_TRACE builds record per-CTA %globaltimer timelines (tools/trace_launches.py).
 //  * Small N: simulate_kernel runs the whole multi-step loop in one cooperative
 //    launch with grid barriers (same decomposition, bitwise-identical results).
 #include "nbody_common.cuh"
