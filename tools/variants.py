@@ -15,6 +15,7 @@ OUT = os.path.join(HERE, "variants")
 VARIANTS = {
     "base": {},
     "trace": {"NB_TRACE": 1},  # per-CTA timelines for tools/trace_launches.py
+    # extra nvcc flags per variant: {"_flags": ["-Xptxas", "..."]}
 }
 
 # GPU optimisation ladder: the reference's ladder axes --
@@ -46,7 +47,9 @@ def build_one(name, defs):
     from paper_2203_08263_b200 import _build as B
     objdir = os.path.join(OUT, name)
     os.makedirs(objdir, exist_ok=True)
-    dflags = [f"-D{k}={v}" for k, v in defs.items()]
+    defs = dict(defs)
+    extra = defs.pop("_flags", [])  # extra nvcc flags for this variant
+    dflags = [f"-D{k}={v}" for k, v in defs.items()] + list(extra)
     objs = []
     for src in B.SOURCES:
         o = os.path.join(objdir, src.replace(".cu", ".o"))
