@@ -4,6 +4,19 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// 1: the e^2 term of the FP64 rsqrt corrections on the FP32/INT pipes
+// (sq_term_f32): 15 DP ops per force interaction instead of 16 (NB_F64_MIXED),
+// 12 per potential pair instead of 13 (NB_DIAG_MIXED).  Measured slower on
+// B200 -- force -7 %, potential -12 % (profiles/variants_r01_f64_mixed.txt):
+// the DP pipe is not the only limit at ~90 % busy (the extra issue slots and
+// register reads cost more than the DP op saves), so both default to off.
+#ifndef NB_F64_MIXED
+#define NB_F64_MIXED 0
+#endif
+#ifndef NB_DIAG_MIXED
+#define NB_DIAG_MIXED 0
+#endif
+
 namespace nb {
 
 // Packed 4-vectors of the system precision: (x, y, z, m) for positions,
@@ -78,6 +91,30 @@ __device__ __forceinline__ double rsqrt_seed(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   return y;
+}
+
+// c*e^2 for the quadratic term of the FP64 rsqrt corrections, computed off the
+// DP pipe.  e = 1 - d2*y0^2 with a MUFU.RSQ64H seed y0 (21 significant bits, so
+// y0^2 is exact) is either 0 or, in magnitude, in [2^-95, 2^-20]: the exact
+// 1 - d2*y0^2 is a nonzero multiple of ulp(d2)*ulp(y0^2) ~ 2^-95 or zero.  For
+// |e| in [2^-255, 1) the top three of the eleven exponent bits are 011, so the
+// 32 bits from the lowest of them down (one funnel shift of the hi:lo pair)
+// read as an FP32 number equal to -|e|*2^128: that exponent bit lands in the
+// sign, the mantissa is truncated to 24 bits, 0 stays 0, and the sign squares
+// away.  The square is formed on the FP32 pipe at that scale and the result, a
+// positive FP32 F = c*e^2*2^128, maps back the same way: the FP64 with bits
+// ((F >> 3) + 0x30000000 : F << 29) is F*2^-128 exactly (0 -> 2^-255, harmless
+// next to 1).  Only the e^2 term is computed this way: it is ~2^-42 of the
+// result, so the FP32 rounding (~2^-22 relative) costs ~2^-64; the linear term
+// stays in FP64.  Per call: one DP op fewer for 2 FMUL + 3 INT ops
+// (SHF.L.W, LEA.HI, IMAD.SHL).
+__device__ __forceinline__ double sq_term_f32(double e, float c) {
+  const unsigned lo = (unsigned)__double2loint(e), hi = (unsigned)__double2hiint(e);
+  const float g = __uint_as_float(__funnelshift_l(lo, hi, 3));  // -|e|*2^128
+  // (g * c*2^-128) is c*|e| (a normal number; the constant itself is an FP32
+  // subnormal, exact for c = 1.875 or 0.375 -- no FTZ on these FMULs).
+  const unsigned f = __float_as_uint((g * (c * 0x1p-128f)) * g);  // c*e^2*2^128
+  return __hiloint2double((int)((f >> 3) + 0x30000000u), (int)(f << 29));
 }
 
 // Launch counter for the gpu_launches claim (host side).

@@ -104,6 +104,11 @@
 #ifndef NB_F64_STAGEWISE
 #define NB_F64_STAGEWISE 1
 #endif
+#if NB_F64_MIXED  // nbody_common.cuh
+#define F64_CORR(e) fma((e), 1.5, nb::sq_term_f32((e), 1.875f))
+#else
+#define F64_CORR(e) ((e) * fma((e), 1.875, 1.5))
+#endif
 
 
 namespace nb {
@@ -447,7 +452,7 @@ struct CoreF64 {
       const double t = y * y;
       const double e = fma(-d2[k], t, 1.0);
       const double my3 = UNI ? t * y : pj.w * (t * y);
-      const double q = e * fma(e, 1.875, 1.5);
+      const double q = F64_CORR(e);
       w[k] = fma(my3, q, my3);
       if (MASK && jj == selfj[k]) w[k] = 0.0;
     }
@@ -470,7 +475,7 @@ struct CoreF64 {
       const double t = y * y;
       const double e = fma(-d2, t, 1.0);
       const double my3 = UNI ? t * y : pj.w * (t * y);
-      const double q = e * fma(e, 1.875, 1.5);
+      const double q = F64_CORR(e);
       double w = fma(my3, q, my3);
       if (MASK && jj == selfj[k]) w = 0.0;
       sx[k] = fma(dx, w, sx[k]);

@@ -137,7 +137,11 @@ __global__ void __launch_bounds__(256) potential_kernel(const V4<R>* pos, int64_
         const double y = rsqrt_seed(d2);
         const double e = fma(-d2, y * y, 1.0);
         const double my = q.w * y;
+#if NB_DIAG_MIXED
+        const double w = fma(my, fma(e, 0.5, sq_term_f32(e, 0.375f)), my);
+#else
         const double w = fma(my, e * fma(e, 0.375, 0.5), my);
+#endif
         acc[k] += (jj == self[k]) ? 0.0 : w;
       }
     }

@@ -5,7 +5,7 @@ pair: 3 DADD, 3 DFMA for d2, 6 for the refined m/r, 1 DADD accumulate; ceiling
 = 148 SM x 64 lanes x 1.965 GHz / 13).  CUDA events, best of 3 after a warm-up.
 usage: python tools/diag_bench.py [CONFIG ...] > profiles/diagnostics_r01.md
 NB_DIAG_LEGACY_LIB=<older libnbody_b200.so> times that library's nb_dev_energy
-(8*n workspace) on the same device states, for a before/after comparison."""
+(its own workspace size; 8*n for the first version) on the same device states, for a before/after comparison."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -29,7 +29,13 @@ def energy(st, eps2):
     if not legacy:
         return st.energy(1.0, eps2)
     out = torch.zeros(6, dtype=torch.float64, device=st.device)
-    ws = torch.empty(8 * st.n, dtype=torch.uint8, device=st.device)
+    if hasattr(LL, "nb_energy_workspace_bytes"):
+        LL.nb_energy_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_int64]
+        LL.nb_energy_workspace_bytes.restype = ctypes.c_int64
+        nbytes = LL.nb_energy_workspace_bytes(st.pbytes, st.n)
+    else:
+        nbytes = 8 * st.n
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=st.device)
     rc = getattr(LL, "nb_dev_energy" + st.sfx)(st.pos_cur.data_ptr(), st.vel.data_ptr(), st.n, 1.0, eps2,
                                                out.data_ptr(), ws.data_ptr(), ws.numel(),
                                                torch.cuda.current_stream().cuda_stream)

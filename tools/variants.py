@@ -15,6 +15,8 @@ OUT = os.path.join(HERE, "variants")
 VARIANTS = {
     "base": {},
     "trace": {"NB_TRACE": 1},  # per-CTA timelines for tools/trace_launches.py
+    # e^2 term of the FP64 rsqrt corrections on the FP32/INT pipes (sq_term_f32)
+    "f64_mixed": {"NB_F64_MIXED": 1, "NB_DIAG_MIXED": 1},
     # extra nvcc flags per variant: {"_flags": ["-Xptxas", "..."]}
 }
 
