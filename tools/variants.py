@@ -17,6 +17,13 @@ VARIANTS = {
     "trace": {"NB_TRACE": 1},  # per-CTA timelines for tools/trace_launches.py
     # e^2 term of the FP64 rsqrt corrections on the FP32/INT pipes (sq_term_f32)
     "f64_mixed": {"NB_F64_MIXED": 1, "NB_DIAG_MIXED": 1},
+    # i-block geometry vs N: K=4 (IB=1024: C2 = 16 whole blocks)
+    # with 1/3 of the weights on LG2/EX2 over 3 source phases (K=8 exceeds 48 KB static smem;
+    # 3 phases do not divide the x16 unroll: the phase test becomes a runtime branch),
+    # and with 3/8 or 1/4 over 4 phases
+    "k4_p3": {"NB_F32_K": 4, "NB_F32_EXP2_MASK": 9, "NB_F32_EXP2_PHASES": 3},
+    "k4_p4_3of8": {"NB_F32_K": 4, "NB_F32_EXP2_MASK": 25, "NB_F32_EXP2_PHASES": 4},
+    "k4_p4_2of8": {"NB_F32_K": 4, "NB_F32_EXP2_MASK": 33, "NB_F32_EXP2_PHASES": 4},
     # extra nvcc flags per variant: {"_flags": ["-Xptxas", "..."]}
 }
 
