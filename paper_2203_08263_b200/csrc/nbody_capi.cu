@@ -40,15 +40,28 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
 
+#ifndef NB_SMALL_MAX_N_F32
+#define NB_SMALL_MAX_N_F32 4096
+#endif
+#ifndef NB_SMALL_MAX_N_F64
+#define NB_SMALL_MAX_N_F64 2560
+#endif
+
 // Bodies up to which nb_dev_simulate runs the whole loop in one persistent
-// cooperative launch (NB_PERSISTENT_MAX_N overrides; 0 disables).
+// cooperative launch (NB_PERSISTENT_MAX_N overrides, read per call; 0 disables).
 int64_t persistent_max_n() {
-  static int64_t v = -1;
-  if (v < 0) {
-    const char* env = getenv("NB_PERSISTENT_MAX_N");
-    v = env ? atoll(env) : 8192;
-  }
-  return v;
+  const char* env = getenv("NB_PERSISTENT_MAX_N");
+  return env ? atoll(env) : 8192;
+}
+
+// Bodies up to which nb_dev_simulate uses the small-N cooperative kernel (source
+// split inside the CTA): NB_SMALL_MAX_N overrides (0 disables; read per call so
+// tests can switch paths), default by precision: the measured crossover with the
+// stream-K persistent kernel (profiles/small_n_r01.md).
+int64_t small_max_n(int precision_bytes) {
+  const char* env = getenv("NB_SMALL_MAX_N");
+  if (env) return atoll(env);
+  return precision_bytes == 4 ? NB_SMALL_MAX_N_F32 : NB_SMALL_MAX_N_F64;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -145,6 +158,24 @@ int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, do
   if (steps < 1) return fail(NB_ERR_ARG, "steps must be >= 1");
   if (!(dt > 0.0)) return fail(NB_ERR_ARG, "dt must be positive");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!events && n <= small_max_n((int)sizeof(R))) {
+    // small N: whole loop in one cooperative launch, source split inside the CTA
+    StepArgs<R> a;
+    int rc = make_step_args<R>(a, pos_a, n, 0, n, 0, n, g, eps2, dt, NB_STEP_FIRST, flags, nullptr, 0, acc4, vel4,
+                               pos_b, ws, ws_bytes, stream, nullptr, 0);
+    if (rc && rc != -1) return rc;
+    if (rc == 0) {
+      cudaError_t e = launch_simulate_small<R>(a, flags & (NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS),
+                                               static_cast<V4<R>*>(pos_a), static_cast<V4<R>*>(pos_b), steps, st);
+      if (e == cudaSuccess) {
+        if (final_in_b) *final_in_b = (steps & 1) ? 1 : 0;
+        return NB_OK;
+      }
+      if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported)
+        return cuda_fail(e, "small_simulate_kernel");
+      cudaGetLastError();  // fall through to the stream-K paths
+    }
+  }
   if (!events && n <= persistent_max_n()) {
     // small N: the whole loop in one cooperative launch (launch-bound otherwise)
     StepArgs<R> a;

@@ -29,8 +29,10 @@
 //    fixup_kernel (programmatic dependent launch, 32-thread CTAs) in fixed CTA
 //    order -- bitwise reproducible run to run -- which then runs the epilogue.
 //  * NB_TRACE builds record per-CTA %globaltimer timelines (tools/trace_launches.py).
-//  * Small N: simulate_kernel runs the whole multi-step loop in one cooperative
-//    launch with grid barriers (same decomposition, bitwise-identical results).
+//  * Small N: the whole multi-step loop runs in one cooperative launch with a
+//    grid barrier per step -- small_simulate_kernel (N <= 4096 FP32 / 2560 FP64:
+//    source split inside the CTA, no global partials) or simulate_kernel (up to
+//    8192: the stream-K decomposition, bitwise identical to per-step launches).
 #include "nbody_common.cuh"
 #include "nbody_kernels.h"
 
@@ -870,6 +872,136 @@ __global__ void __launch_bounds__(T, MINB) simulate_kernel(StepArgs<typename Cor
   }
 }
 
+// ---------------------------------------------------------------- small-N cooperative simulate
+// For a few thousand bodies (C1: N = 1024) the stream-K pass spreads one or two
+// i-blocks over up to 148 CTAs, and every step then writes and re-reads ~2 MB
+// of FP64 partial slots (C1: ~5 us each way, profiles/trace_C1_r01.md).  This
+// kernel keeps the source split INSIDE the CTA instead: a CTA owns 2*PPW
+// targets (PPW pairs; PPW = 8 or 4), each of its 8 warps holds all of them on
+// PPW lanes x G = 32/PPW lane groups, so the CTA runs S = 8*G source splits;
+// each thread runs one target pair over its split, and the S partial sums are
+// combined by a shuffle butterfly over the lane groups and a fixed-order pass
+// over the 8 warps -- no global partials, no fixup, bitwise reproducible.  Each
+// step stages all N bodies into shared memory split-major (split s holds
+// j = s, s+S, ... contiguously, padded so a warp's lane groups read disjoint
+// banks), then one grid barrier.  Same Core arithmetic as the main kernel (the
+// FP32 split is <= N/S terms in FP32 before the FP64 sums).
+constexpr int SN_T = 256;  // threads per CTA (8 warps)
+
+// Bodies per split in shared memory: ceil(N/S) rounded up to 1 mod 8, so the
+// splits of one warp's lane groups start 4 banks apart (FP32 bodies; FP64 ones
+// take two 16-byte halves, 8 banks apart).
+__host__ __device__ inline int64_t small_split_stride(int64_t n, int splits) {
+  const int64_t L = (n + splits - 1) / splits;
+  return L + (((1 - L) % 8) + 8) % 8;
+}
+
+template <bool M, bool U> struct SmallF32 : CoreF32<2, M, 4, U> { static constexpr bool MASK_SELF = M; };
+template <bool M, bool U> struct SmallF64 : CoreF64<2, M, 4, U> { static constexpr bool MASK_SELF = M; };
+
+template <class Core, int PPW>
+__global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename Core::R> a,
+                                                              V4<typename Core::R>* pos_a,
+                                                              V4<typename Core::R>* pos_b, int64_t steps,
+                                                              int64_t L) {
+  using R = typename Core::R;
+  using B = V4<R>;
+  constexpr int G = 32 / PPW;        // lane groups per warp
+  constexpr int S = (SN_T / 32) * G; // source splits per CTA
+  constexpr int TB = 2 * PPW;        // target bodies per CTA
+  extern __shared__ __align__(128) unsigned char sn_smem[];
+  B* sp = reinterpret_cast<B*>(sn_smem);                              // S * L bodies
+  float* slm = reinterpret_cast<float*>(sp + S * L);                  // log2(m_j), same layout
+  double* ssum = reinterpret_cast<double*>(slm + (Core::NEEDS_LM ? S * L : 0));
+  double* red = ssum + Core::SMEM_SUMS * SN_T;                        // [8 warps][TB targets][3]
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pr = lane % PPW, sub = lane / PPW;
+  const int s = warp * G + sub;  // this thread's source split: j = s + S*jj
+  const int64_t n = a.n_all;
+  const int64_t i0 = blockIdx.x * (int64_t)TB + 2 * pr;
+  const int cnt = s < n ? (int)((n - s + S - 1) / S) : 0;
+  auto slot = [&](int64_t j) { return (j % S) * L + j / S; };
+
+  Core core;
+  core.init(a.eps2, ssum + tid, SN_T);
+  core.lmt = slm + s * L;
+  if (Core::MASK_SELF) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int64_t i = i0 + k;
+      core.selfj[k] = (i < n && (int)(i % S) == s) ? (int)(i / S) : -1;
+    }
+  }
+  for (int64_t st = 0; st <= steps; ++st) {
+    a.mode = st == 0 ? NB_STEP_MODE_FIRST : (st < steps ? NB_STEP_MODE_KICK_DRIFT : NB_STEP_MODE_FINAL);
+    a.pos = (st & 1) ? pos_b : pos_a;
+    a.pos_next = (st & 1) ? pos_a : pos_b;
+    for (int64_t j = tid; j < n; j += SN_T) {  // positions moved last step: coherent loads
+      const B b = ld4_cg(a.pos + j);
+      sp[slot(j)] = b;
+      if (Core::NEEDS_LM) slm[slot(j)] = lg2_mufu((float)b.w);
+    }
+    __syncthreads();
+    const int64_t ia = i0 < n ? i0 : n - 1, ib = i0 + 1 < n ? i0 + 1 : n - 1;
+    core.set_pair(0, sp[slot(ia)], sp[slot(ib)]);
+    core.zero_sums();
+    core.begin_tile();
+    const B* tb = sp + s * L;
+    int jj = 0;
+#pragma unroll 1
+    for (; jj + 4 <= cnt; jj += 4) {
+      core.interact(tb[jj], jj);
+      core.interact(tb[jj + 1], jj + 1);
+      core.interact(tb[jj + 2], jj + 2);
+      core.interact(tb[jj + 3], jj + 3);
+    }
+#pragma unroll 1
+    for (; jj < cnt; ++jj) core.interact(tb[jj], jj);
+    core.end_tile();
+    // S splits -> 1: butterfly over the lane groups (a + b == b + a, so every
+    // lane ends with the same bits), then the 8 warps in ascending order.
+    double v[6];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      v[2 * d] = core.sum(d, 0);
+      v[2 * d + 1] = core.sum(d, 1);
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+      for (int x = PPW; x < 32; x *= 2) v[q] += __shfl_xor_sync(0xffffffffu, v[q], x);
+    if (sub == 0) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        red[(warp * TB + 2 * pr) * 3 + d] = v[2 * d];
+        red[(warp * TB + 2 * pr + 1) * 3 + d] = v[2 * d + 1];
+      }
+    }
+    __syncthreads();
+    if (tid < TB) {
+      const int64_t il = blockIdx.x * (int64_t)TB + tid;
+      double t[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int w = 0; w < SN_T / 32; ++w)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) t[d] += red[(w * TB + tid) * 3 + d];
+      if (il < n) finalize_body<R>(a, il, t[0], t[1], t[2]);
+    }
+    grid.sync();  // new positions visible; nobody still reads the old buffer or red
+  }
+}
+
+template <typename R>
+int64_t small_smem_bytes(int64_t n, int ppw, bool needs_lm) {
+  const int splits = (SN_T / 32) * (32 / ppw);
+  const int64_t L = small_split_stride(n, splits);
+  const int64_t sums = sizeof(R) == 4 ? 6 : 1;  // Core::SMEM_SUMS doubles per thread
+  return splits * L * (int64_t)sizeof(V4<R>) + (needs_lm ? splits * L * 4 : 0) + sums * SN_T * 8 +
+         (SN_T / 32) * 2 * ppw * 3 * 8;
+}
+
 // ---------------------------------------------------------------- configurations
 // Both precisions: 256 threads x 6 target bodies = 1536-body i-blocks, 256-body
 // source tiles (FP32: 3 packed FFMA2 pairs per thread).
@@ -1055,6 +1187,52 @@ cudaError_t launch_simulate_persistent(StepArgs<R> a, int flags, V4<R>* pos_a, V
   return e;
 }
 
+template <class Core, int PPW>
+static const void* small_fn() {
+  return reinterpret_cast<const void*>(&small_simulate_kernel<Core, PPW>);
+}
+template <typename R, int PPW>
+static const void* small_fn(bool mask_self, bool uni) {
+  if constexpr (sizeof(R) == 4) {
+    if (mask_self) return uni ? small_fn<SmallF32<true, true>, PPW>() : small_fn<SmallF32<true, false>, PPW>();
+    return uni ? small_fn<SmallF32<false, true>, PPW>() : small_fn<SmallF32<false, false>, PPW>();
+  } else {
+    if (mask_self) return uni ? small_fn<SmallF64<true, true>, PPW>() : small_fn<SmallF64<true, false>, PPW>();
+    return uni ? small_fn<SmallF64<false, true>, PPW>() : small_fn<SmallF64<false, false>, PPW>();
+  }
+}
+
+// 8 targets per CTA (twice the CTAs) up to N = 3072 (FP32) / 1184 (FP64), else
+// 16: the measured crossovers (profiles/small_n_r01.md; NB_SMALL_PPW=4|8 forces one).
+template <typename R>
+cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b, int64_t steps,
+                                  cudaStream_t stream) {
+  const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
+  a.uniform_mass = uni ? 1 : 0;
+  const int64_t n = a.n_all;
+  int dev = 0, per_sm = 0, sms = 0, smem_max = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int ppw = n <= (sizeof(R) == 4 ? 3072 : 1184) ? 4 : 8;
+  if (const char* env = getenv("NB_SMALL_PPW")) ppw = atoi(env) == 4 ? 4 : 8;
+  const void* fn = ppw == 4 ? small_fn<R, 4>(mask_self, uni) : small_fn<R, 8>(mask_self, uni);
+  bool needs_lm = false;
+  if constexpr (sizeof(R) == 4) needs_lm = !uni && SmallF32<false, false>::NEEDS_LM;
+  const int64_t smem = small_smem_bytes<R>(n, ppw, needs_lm);
+  if (smem > smem_max) return cudaErrorCooperativeLaunchTooLarge;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SN_T, (size_t)smem);
+  const int64_t grid = (n + 2 * ppw - 1) / (2 * ppw);
+  if (grid > (int64_t)per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
+  int64_t L = small_split_stride(n, (SN_T / 32) * (32 / ppw));
+  void* args[] = {&a, &pos_a, &pos_b, &steps, &L};
+  e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(SN_T), args, (size_t)smem, stream);
+  count_launch();
+  return e;
+}
+
 #if NB_TRACE
 int trace_setup(void* buf, int64_t cap) {
   unsigned long long* p = static_cast<unsigned long long*>(buf);
@@ -1089,5 +1267,8 @@ template cudaError_t launch_simulate_persistent<double>(StepArgs<double>, int, V
                                                        cudaStream_t);
 template int64_t step_workspace_bytes<float>(int64_t);
 template int64_t step_workspace_bytes<double>(int64_t);
+template cudaError_t launch_simulate_small<float>(StepArgs<float>, int, V4<float>*, V4<float>*, int64_t, cudaStream_t);
+template cudaError_t launch_simulate_small<double>(StepArgs<double>, int, V4<double>*, V4<double>*, int64_t,
+                                                   cudaStream_t);
 
 }  // namespace nb

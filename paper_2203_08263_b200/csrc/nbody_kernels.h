@@ -51,6 +51,11 @@ template <typename R> int64_t step_workspace_bytes(int64_t n_i);
 // Whole simulate loop (steps drift steps + the final kick) in one cooperative launch.
 template <typename R> cudaError_t launch_simulate_persistent(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b,
                                                              int64_t steps, cudaStream_t s);
+// Small N: the whole simulate loop in one cooperative launch with the source split
+// inside each CTA (no global partials); cudaErrorCooperativeLaunchTooLarge when
+// the grid or its shared memory does not fit.
+template <typename R> cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b,
+                                                        int64_t steps, cudaStream_t s);
 // Byte offset of the slot area inside the workspace (a 256-byte-aligned header).
 inline int64_t counters_bytes(int64_t n_iblocks) { return ((n_iblocks * 4 + 255) / 256) * 256; }
 
