@@ -10,6 +10,8 @@ import paper_2203_08263_b200 as nb
 from paper_2203_08263_b200.device import DeviceState, kernel_flags
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+NS = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else \
+    [256, 512, 1024, 1536, 2048, 2368, 3072, 4096, 6144, 8192, 16384, 32768]
 PATHS = {"small": ("1000000000", "0", ""), "small/8": ("1000000000", "0", "4"), "small/16": ("1000000000", "0", "8"),
          "persistent": ("0", "1000000000", ""), "per-launch": ("0", "0", "")}
 
@@ -40,7 +42,7 @@ print("`small` = the small-N kernel with its default CTA size, `small/8`, `small
 print("| precision | N | small (µs) | small/8 | small/16 | persistent (µs) | per-launch (µs) | best | interactions/s (best) |")
 print("|---|---|---|---|---|---|---|---|---|")
 for prec in ("double", "single"):
-    for n in (256, 512, 1024, 1536, 2048, 2368, 3072, 4096, 6144, 8192):
+    for n in NS:
         s = nb.uniform_cube(n, 0, nb.Precision(prec))
         dt_ = s.precision.dtype
         st = DeviceState(s.position_matrix().astype(dt_), np.stack(s.velocities, 1), s.masses, dt_)
