@@ -162,9 +162,15 @@ int nb_dev_step_p2p_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_
                         void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Device-resident kernels.simulate for one GPU: `steps` fused steps plus the final
- * evaluation and kick (steps+1 launches), ping-ponging pos4_a <-> pos4_b.  On
- * return (stream-ordered) the final positions are in pos4_a if steps is even,
- * else in pos4_b; *final_in_b reports which (may be NULL). */
+ * evaluation and kick (steps+1 force evaluations), ping-ponging pos4_a <-> pos4_b.
+ * On return (stream-ordered) the final positions are in pos4_a if steps is even,
+ * else in pos4_b; *final_in_b reports which (may be NULL).  Small N runs the whole
+ * loop in one cooperative launch: N <= 4096 (FP32) / 2560 (FP64) with the source
+ * split inside each CTA (environment NB_SMALL_MAX_N overrides, 0 disables; its
+ * summation order differs from the per-step path, results agree within the
+ * parity tolerances), up to 8192 with the per-step decomposition (bitwise equal
+ * to per-step launches; NB_PERSISTENT_MAX_N overrides).  Larger N: one launch
+ * (plus a split-block fixup launch) per force evaluation. */
 int nb_dev_simulate_f32(void* pos4_a, void* pos4_b, void* vel4, void* acc4, int64_t n,
                         double g, double dt, double eps2, int64_t steps, int flags,
                         void* workspace, int64_t workspace_bytes, void* stream,
