@@ -922,7 +922,11 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
   const int64_t n = a.n_all;
   const int64_t i0 = blockIdx.x * (int64_t)TB + 2 * pr;
   const int cnt = s < n ? (int)((n - s + S - 1) / S) : 0;
-  auto slot = [&](int64_t j) { return (j % S) * L + j / S; };
+  auto slot = [&](int64_t j) {
+    const int64_t q = (j % S) * L + j / S;
+    NB_DCHECK(j >= 0 && j < n && q >= 0 && q < S * L);
+    return q;
+  };
 
   Core core;
   core.init(a.eps2, ssum + tid, SN_T);
@@ -949,6 +953,7 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
     core.zero_sums();
     core.begin_tile();
     const B* tb = sp + s * L;
+    NB_DCHECK(cnt >= 0 && cnt <= L);
     int jj = 0;
 #pragma unroll 1
     for (; jj + 4 <= cnt; jj += 4) {
@@ -975,6 +980,7 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
     if (sub == 0) {
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
+        NB_DCHECK((warp * TB + 2 * pr + 1) * 3 + d < (SN_T / 32) * TB * 3);
         red[(warp * TB + 2 * pr) * 3 + d] = v[2 * d];
         red[(warp * TB + 2 * pr + 1) * 3 + d] = v[2 * d + 1];
       }
