@@ -203,6 +203,25 @@ int nb_dev_pack_f64(const void* x, const void* y, const void* z, const void* w, 
 int nb_dev_unpack_f32(const void* in4, int64_t n, void* x, void* y, void* z, void* stream);
 int nb_dev_unpack_f64(const void* in4, int64_t n, void* x, void* y, void* z, void* stream);
 
+/* The same conversion fused with its transfer, for simulate()'s column staging:
+ * one call each way (small N is host-latency-bound).  Column block layout, in
+ * elements of the system precision: x, y, z, m of all n bodies at 0, n, 2n, 3n,
+ * then vx, vy, vz of the n_i owned rows at 4n, 4n + ni, 4n + 2ni with
+ * ni = max(n_i, 1) -- 4n + 3ni elements.  load: H2D of the whole block from
+ * host_cols (pinned for an asynchronous copy), then pos4 (n rows, masses in .w)
+ * and vel4 (n_i rows) packed from it; asynchronous.  store: pos4 and vel4
+ * unpacked into dev_cols (the mass column is left as is), D2H of the x, y, z
+ * and vx, vy, vz columns into the same places of host_cols, and a synchronize
+ * of `stream` before returning. */
+int nb_dev_load_cols_f32(const void* host_cols, void* dev_cols, int64_t n, int64_t n_i,
+                         void* pos4, void* vel4, void* stream);
+int nb_dev_load_cols_f64(const void* host_cols, void* dev_cols, int64_t n, int64_t n_i,
+                         void* pos4, void* vel4, void* stream);
+int nb_dev_store_cols_f32(const void* pos4, const void* vel4, int64_t n, int64_t n_i,
+                          void* dev_cols, void* host_cols, void* stream);
+int nb_dev_store_cols_f64(const void* pos4, const void* vel4, int64_t n, int64_t n_i,
+                          void* dev_cols, void* host_cols, void* stream);
+
 /* Stand-alone update kernels on packed arrays (n entries each): the kick-drift
  * of step_soa (_accel_cy.pyx:205-237) in place, and the trapezoidal kick of
  * _kick (kernels/__init__.py:220-227): v += (a_new - a_old) * real(factor). */

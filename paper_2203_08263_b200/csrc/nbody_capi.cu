@@ -422,6 +422,46 @@ int dev_unpack(const void* in4, int64_t n, void* x, void* y, void* z, void* stre
   return NB_OK;
 }
 
+// Column block of simulate()'s staging (header: nb_dev_load_cols_*).
+template <typename R>
+int dev_load_cols(const void* host_cols, void* dev_cols, int64_t n, int64_t n_i, void* pos4, void* vel4,
+                  void* stream) {
+  if (n < 1 || n_i < 0 || n_i > n) return fail(NB_ERR_ARG, "need n >= 1 and 0 <= n_i <= n");
+  if (!host_cols || !dev_cols || !pos4 || (n_i && !vel4)) return fail(NB_ERR_ARG, "null pointer");
+  if (!aligned16(pos4) || (n_i && !aligned16(vel4))) return fail(NB_ERR_ARG, "pos4/vel4 must be 16-byte aligned");
+  if (cudaError_t be = bind_device_of(pos4)) return cuda_fail(be, "pos4 is not a device pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t ni = n_i > 0 ? n_i : 1;
+  R* d = static_cast<R*>(dev_cols);
+  NB_CUDA(cudaMemcpyAsync(d, host_cols, (size_t)(4 * n + 3 * ni) * sizeof(R), cudaMemcpyHostToDevice, st));
+  NB_CUDA(launch_pack_soa<R>(d, d + n, d + 2 * n, d + 3 * n, static_cast<V4<R>*>(pos4), n, st));
+  if (n_i)
+    NB_CUDA(launch_pack_soa<R>(d + 4 * n, d + 4 * n + ni, d + 4 * n + 2 * ni, nullptr, static_cast<V4<R>*>(vel4),
+                               n_i, st));
+  return NB_OK;
+}
+
+template <typename R>
+int dev_store_cols(const void* pos4, const void* vel4, int64_t n, int64_t n_i, void* dev_cols, void* host_cols,
+                   void* stream) {
+  if (n < 1 || n_i < 0 || n_i > n) return fail(NB_ERR_ARG, "need n >= 1 and 0 <= n_i <= n");
+  if (!host_cols || !dev_cols || !pos4 || (n_i && !vel4)) return fail(NB_ERR_ARG, "null pointer");
+  if (cudaError_t be = bind_device_of(pos4)) return cuda_fail(be, "pos4 is not a device pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t ni = n_i > 0 ? n_i : 1;
+  R* d = static_cast<R*>(dev_cols);
+  NB_CUDA(launch_unpack_soa<R>(static_cast<const V4<R>*>(pos4), d, d + n, d + 2 * n, n, st));
+  if (n_i)
+    NB_CUDA(launch_unpack_soa<R>(static_cast<const V4<R>*>(vel4), d + 4 * n, d + 4 * n + ni, d + 4 * n + 2 * ni,
+                                 n_i, st));
+  R* h = static_cast<R*>(host_cols);
+  NB_CUDA(cudaMemcpyAsync(h, d, (size_t)(3 * n) * sizeof(R), cudaMemcpyDeviceToHost, st));  // x, y, z
+  if (n_i)
+    NB_CUDA(cudaMemcpyAsync(h + 4 * n, d + 4 * n, (size_t)(3 * ni) * sizeof(R), cudaMemcpyDeviceToHost, st));
+  NB_CUDA(cudaStreamSynchronize(st));
+  return NB_OK;
+}
+
 template <typename R>
 int dev_drift(void* pos4, void* vel4, const void* acc4, int64_t n, double dt, void* stream) {
   if (n < 0) return fail(NB_ERR_ARG, "n must be >= 0");
@@ -593,6 +633,22 @@ int nb_dev_unpack_f32(const void* in4, int64_t n, void* x, void* y, void* z, voi
 }
 int nb_dev_unpack_f64(const void* in4, int64_t n, void* x, void* y, void* z, void* stream) {
   return dev_unpack<double>(in4, n, x, y, z, stream);
+}
+int nb_dev_load_cols_f32(const void* host_cols, void* dev_cols, int64_t n, int64_t n_i, void* pos4, void* vel4,
+                         void* stream) {
+  return dev_load_cols<float>(host_cols, dev_cols, n, n_i, pos4, vel4, stream);
+}
+int nb_dev_load_cols_f64(const void* host_cols, void* dev_cols, int64_t n, int64_t n_i, void* pos4, void* vel4,
+                         void* stream) {
+  return dev_load_cols<double>(host_cols, dev_cols, n, n_i, pos4, vel4, stream);
+}
+int nb_dev_store_cols_f32(const void* pos4, const void* vel4, int64_t n, int64_t n_i, void* dev_cols,
+                          void* host_cols, void* stream) {
+  return dev_store_cols<float>(pos4, vel4, n, n_i, dev_cols, host_cols, stream);
+}
+int nb_dev_store_cols_f64(const void* pos4, const void* vel4, int64_t n, int64_t n_i, void* dev_cols,
+                          void* host_cols, void* stream) {
+  return dev_store_cols<double>(pos4, vel4, n, n_i, dev_cols, host_cols, stream);
 }
 int nb_dev_drift_f32(void* pos4, void* vel4, const void* acc4, int64_t n, double dt, void* stream) {
   return dev_drift<float>(pos4, vel4, acc4, n, dt, stream);

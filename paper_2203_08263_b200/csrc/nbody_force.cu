@@ -1216,25 +1216,49 @@ cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>*
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
   const int64_t n = a.n_all;
-  int dev = 0, per_sm = 0, sms = 0, smem_max = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   int ppw = n <= (sizeof(R) == 4 ? 3072 : 1184) ? 4 : 8;
   if (const char* env = getenv("NB_SMALL_PPW")) ppw = atoi(env) == 4 ? 4 : 8;
   const void* fn = ppw == 4 ? small_fn<R, 4>(mask_self, uni) : small_fn<R, 8>(mask_self, uni);
   bool needs_lm = false;
   if constexpr (sizeof(R) == 4) needs_lm = !uni && SmallF32<false, false>::NEEDS_LM;
   const int64_t smem = small_smem_bytes<R>(n, ppw, needs_lm);
-  if (smem > smem_max) return cudaErrorCooperativeLaunchTooLarge;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SN_T, (size_t)smem);
+  // Host-side launch preparation is on simulate()'s critical path at small N:
+  // the co-resident capacity is cached per (device, kernel, shared-memory size)
+  // and the opt-in shared-memory limit per (device, kernel) only ever raised.
+  struct Cap { int dev; const void* fn; int64_t smem; int capacity; };
+  struct Opt { int dev; const void* fn; int64_t smem; };
+  static Cap caps[64];
+  static Opt opts[32];
+  static int n_caps = 0, n_opts = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Opt* opt = nullptr;
+  for (int k = 0; k < n_opts; ++k)
+    if (opts[k].dev == dev && opts[k].fn == fn) opt = &opts[k];
+  if (!opt || opt->smem < smem) {
+    int smem_max = 0;
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (smem > smem_max) return cudaErrorCooperativeLaunchTooLarge;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (!opt && n_opts < 32) opt = &opts[n_opts++];
+    if (opt) *opt = Opt{dev, fn, smem};
+  }
+  int capacity = -1;
+  for (int k = 0; k < n_caps; ++k)
+    if (caps[k].dev == dev && caps[k].fn == fn && caps[k].smem == smem) capacity = caps[k].capacity;
+  if (capacity < 0) {
+    int per_sm = 0, sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SN_T, (size_t)smem);
+    capacity = per_sm * sms;
+    if (n_caps < 64) caps[n_caps++] = Cap{dev, fn, smem, capacity};
+  }
   const int64_t grid = (n + 2 * ppw - 1) / (2 * ppw);
-  if (grid > (int64_t)per_sm * sms) return cudaErrorCooperativeLaunchTooLarge;
+  if (grid > (int64_t)capacity) return cudaErrorCooperativeLaunchTooLarge;
   int64_t L = small_split_stride(n, (SN_T / 32) * (32 / ppw));
   void* args[] = {&a, &pos_a, &pos_b, &steps, &L};
-  e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(SN_T), args, (size_t)smem, stream);
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(SN_T), args, (size_t)smem, stream);
   count_launch();
   return e;
 }

@@ -19,6 +19,7 @@ HBM layout (one GPU, or one i-shard of a multi-GPU run):
 from __future__ import annotations
 
 import ctypes
+import math
 from typing import Optional, Tuple
 
 import numpy as np
@@ -33,26 +34,34 @@ __all__ = ["DeviceState", "needs_self_mask", "kernel_flags", "pack_bodies", "TOR
 TORCH_DTYPE = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
 
 
-def needs_self_mask(masses: np.ndarray, eps2: float, dtype) -> bool:
-    """True when the self pair must be excluded explicitly: (real)eps2 == 0
-    (0*inf at j == i, the case pinned by pkg/tests/test_kernels.py:51-55), or a
-    self term m*eps2^-1.5 that would overflow the system precision."""
-    dtype = np.dtype(dtype)
+def _self_mask(mmax: float, eps2: float, dtype: np.dtype) -> bool:
     e = float(dtype.type(eps2))
     if not e > 0.0:
         return True
     big = 1e30 if dtype == np.float32 else 1e300
-    mmax = float(np.max(masses)) if masses.size else 0.0
-    return not (mmax * (1.0 / e) / np.sqrt(e) < big)
+    return not (mmax * (1.0 / e) / math.sqrt(e) < big)
+
+
+def needs_self_mask(masses: np.ndarray, eps2: float, dtype) -> bool:
+    """True when the self pair must be excluded explicitly: (real)eps2 == 0
+    (0*inf at j == i, the case pinned by pkg/tests/test_kernels.py:51-55), or a
+    self term m*eps2^-1.5 that would overflow the system precision."""
+    m = np.asarray(masses)
+    return _self_mask(float(m.max()) if m.size else 0.0, eps2, np.dtype(dtype))
 
 
 def kernel_flags(masses: np.ndarray, eps2: float, dtype, allow_uniform: bool = True) -> int:
     """nb_dev_step flags for a system: NB_FLAG_EXCLUDE_SELF when the self pair
     must be masked, NB_FLAG_UNIFORM_MASS when every mass is identical (m is then
-    applied once per body; C5's Plummer sphere has m = 1/N for all bodies)."""
+    applied once per body; C5's Plummer sphere has m = 1/N for all bodies).
+    (Masses are finite and positive -- validated at the boundary -- so
+    max == min is "all equal".)"""
     m = np.asarray(masses)
-    flags = NB_FLAG_EXCLUDE_SELF if needs_self_mask(m, eps2, dtype) else 0
-    if allow_uniform and m.size and bool(np.all(m == m[0])):
+    if not m.size:
+        return NB_FLAG_EXCLUDE_SELF if _self_mask(0.0, eps2, np.dtype(dtype)) else 0
+    mmax, mmin = float(m.max()), float(m.min())
+    flags = NB_FLAG_EXCLUDE_SELF if _self_mask(mmax, eps2, np.dtype(dtype)) else 0
+    if allow_uniform and mmax == mmin:
         flags |= NB_FLAG_UNIFORM_MASS
     return flags
 
@@ -113,28 +122,27 @@ class DeviceState:
         """Column staging reused by every load()/readback: 7 columns (x, y, z, m of
         all N bodies; vx, vy, vz of the n_i owned ones) in pinned host memory and on
         the device, so each transfer is ONE contiguous copy and the (de)interleave
-        to the packed rows runs on the GPU (nb_dev_pack / nb_dev_unpack)."""
+        to the packed rows runs on the GPU (nb_dev_load_cols / nb_dev_store_cols)."""
         tdt = TORCH_DTYPE[self.dtype]
         ncol = 4 * self.n + 3 * max(self.n_i, 1)
         self._h_cols = torch.empty(ncol, dtype=tdt, pin_memory=True)
         self._d_cols = torch.empty(ncol, dtype=tdt, device=self.device)
+        # fixed for the life of the state: the numpy view and the raw pointers
+        self._h_np = self._h_cols.numpy()
+        self._cols_ptrs = (self._h_cols.data_ptr(), self._d_cols.data_ptr())
         self._h_out = torch.empty((self.n, 4), dtype=tdt, pin_memory=True)
         self._h2d_done = None
-
-    def _col(self, t: torch.Tensor, k: int) -> int:
-        """Device/host address of staging column k (0-3: x, y, z, m; 4-6: vx, vy, vz)."""
-        off = k * self.n if k < 4 else 4 * self.n + (k - 4) * max(self.n_i, 1)
-        return t.data_ptr() + off * self.pbytes
+        self._h2d_pending = False
 
     def load(self, positions, velocities, masses: np.ndarray) -> None:
         """(Re)initialise the resident state from host data -- (N,3) arrays or
         (x, y, z) column tuples: contiguous column writes into the pinned staging,
         one asynchronous H2D and two pack launches on the current stream."""
-        if self._h2d_done is not None:
+        if self._h2d_pending:
             self._h2d_done.synchronize()  # staging still feeding the previous copy
         self.masses = np.ascontiguousarray(masses, dtype=self.dtype)
         n, ni = self.n, self.n_i
-        h = self._h_cols.numpy()
+        h = self._h_np
         lo, hi = self.i_begin, self.i_begin + ni
         if not isinstance(positions, (tuple, list)):
             positions = tuple(np.asarray(positions)[:, k] for k in range(3))
@@ -143,33 +151,28 @@ class DeviceState:
             h[k * n:(k + 1) * n] = positions[k]
             h[4 * n + k * max(ni, 1): 4 * n + k * max(ni, 1) + ni] = velocities[k][lo:hi]
         h[3 * n:4 * n] = self.masses
-        self._d_cols.copy_(self._h_cols, non_blocking=True)
-        self._h2d_done = torch.cuda.Event()
+        # one native call: H2D of the column block + the two pack launches
+        hp, dp = self._cols_ptrs
+        _native.call("nb_dev_load_cols" + self.sfx, hp, dp, n, ni, self.pos_a.data_ptr(), self.vel.data_ptr(),
+                     self.stream_ptr())
+        if self._h2d_done is None:
+            self._h2d_done = torch.cuda.Event()
         self._h2d_done.record()
-        d, s = self._d_cols, self.stream_ptr()
-        _native.call("nb_dev_pack" + self.sfx, self._col(d, 0), self._col(d, 1), self._col(d, 2),
-                     self._col(d, 3), n, self.pos_a.data_ptr(), s)
-        if ni:
-            _native.call("nb_dev_pack" + self.sfx, self._col(d, 4), self._col(d, 5), self._col(d, 6), None, ni,
-                         self.vel.data_ptr(), s)
+        self._h2d_pending = True
         self.cur_is_a = True
 
     def columns_host(self):
         """Current positions (x, y, z of all N) and velocities (of the n_i owned
-        rows) as six fresh contiguous host arrays: two unpack launches, one
-        contiguous D2H into the pinned staging, six memcpys."""
-        d, s = self._d_cols, self.stream_ptr()
+        rows) as six fresh contiguous host arrays: one native call (two unpack
+        launches, the D2H into the pinned staging, a stream sync), six memcpys."""
         n, ni = self.n, self.n_i
-        _native.call("nb_dev_unpack" + self.sfx, self.pos_cur.data_ptr(), n, self._col(d, 0), self._col(d, 1),
-                     self._col(d, 2), s)
-        if ni:
-            _native.call("nb_dev_unpack" + self.sfx, self.vel.data_ptr(), ni, self._col(d, 4), self._col(d, 5),
-                         self._col(d, 6), s)
-        if self._h2d_done is not None:
-            self._h2d_done.synchronize()
-            self._h2d_done = None
-        self._h_cols.copy_(self._d_cols)  # synchronizes the stream
-        h = self._h_cols.numpy()
+        # (a pending H2D from the staging is earlier on the same stream: no wait needed)
+        self._h2d_pending = False
+        # one native call: the two unpack launches + D2H of the block + stream sync
+        hp, dp = self._cols_ptrs
+        _native.call("nb_dev_store_cols" + self.sfx, self.pos_cur.data_ptr(), self.vel.data_ptr(), n, ni, dp, hp,
+                     self.stream_ptr())
+        h = self._h_np
         pos = tuple(np.array(h[k * n:(k + 1) * n]) for k in range(3))
         vel = tuple(np.array(h[4 * n + k * max(ni, 1): 4 * n + k * max(ni, 1) + ni]) for k in range(3))
         return pos, vel

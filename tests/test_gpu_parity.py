@@ -792,8 +792,8 @@ def test_energy_diagnostics(oracle, n, prec, eps2):
 @pytest.mark.parametrize("prec", ["double", "single"])
 @pytest.mark.parametrize("shard", [False, True])
 def test_column_staging_roundtrip(prec, shard):
-    """DeviceState.load (column staging, nb_dev_pack) and columns_host
-    (nb_dev_unpack): packed rows equal the input bit for bit from either input
+    """DeviceState.load (column staging, nb_dev_load_cols) and columns_host
+    (nb_dev_store_cols): packed rows equal the input bit for bit from either input
     form, and the columns come back unchanged -- for a sharded state only the
     owned velocity rows."""
     from paper_2203_08263_b200.device import DeviceState
