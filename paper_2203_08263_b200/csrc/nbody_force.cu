@@ -489,6 +489,43 @@ struct CoreF64 {
 };
 
 // ---------------------------------------------------------------- epilogue
+// a = real(G * sum) and the reference's update of one body from its previous
+// velocity v, previous acceleration ap and current position p (all loaded by
+// the caller): exactly the reference's rounding sequence (no contraction).  On
+// return v and ap hold the new velocity and acceleration (also stored).
+template <typename R>
+__device__ __forceinline__ void integrate_body(const StepArgs<R>& a, int64_t il, double tx, double ty, double tz,
+                                               V4<R>& v, V4<R>& ap, V4<R> p) {
+  // Uniform-mass kernels left m_j out of every term: apply it once here.
+  const double gm = a.uniform_mass ? a.g * (double)a.pos[0].w : a.g;
+  const R ax = (R)(tx * gm), ay = (R)(ty * gm), az = (R)(tz * gm);
+  V4<R> an;
+  an.x = ax; an.y = ay; an.z = az; an.w = R(0);
+  if (a.mode != NB_STEP_MODE_ACCEL) {
+    if (a.mode != NB_STEP_MODE_FIRST) {  // trapezoidal kick, kernels/__init__.py:223-227
+      v.x = add_rn(v.x, mul_rn(sub_rn(ax, ap.x), a.f));
+      v.y = add_rn(v.y, mul_rn(sub_rn(ay, ap.y), a.f));
+      v.z = add_rn(v.z, mul_rn(sub_rn(az, ap.z), a.f));
+    }
+    if (a.mode != NB_STEP_MODE_FINAL) {  // kick-drift, _accel_cy.pyx:218-226
+      const int64_t ig = a.i_begin + il;
+      const R dvx = mul_rn(ax, a.dt), dvy = mul_rn(ay, a.dt), dvz = mul_rn(az, a.dt);
+      p.x = add_rn(p.x, mul_rn(add_rn(v.x, mul_rn(a.half, dvx)), a.dt));
+      p.y = add_rn(p.y, mul_rn(add_rn(v.y, mul_rn(a.half, dvy)), a.dt));
+      p.z = add_rn(p.z, mul_rn(add_rn(v.z, mul_rn(a.half, dvz)), a.dt));
+      NB_DCHECK(ig >= 0 && ig < a.n_all && il >= 0 && il < a.n_i);
+      st4(a.pos_next + ig, p);
+      for (int q = 0; q < a.n_peers; ++q) st4(a.peers[q] + ig, p);  // NVLink peer stores
+      v.x = add_rn(v.x, dvx);
+      v.y = add_rn(v.y, dvy);
+      v.z = add_rn(v.z, dvz);
+    }
+    st4(a.vel + il, v);
+  }
+  st4(a.acc + il, an);
+  ap = an;
+}
+
 template <typename R>
 __device__ __forceinline__ void finalize_body(const StepArgs<R>& a, int64_t il, double tx,
                                               double ty, double tz) {
@@ -504,36 +541,13 @@ __device__ __forceinline__ void finalize_body(const StepArgs<R>& a, int64_t il, 
     a.carry[2 * a.n_i + il] = tz;
     return;
   }
-  // Uniform-mass kernels left m_j out of every term: apply it once here.
-  const double gm = a.uniform_mass ? a.g * (double)a.pos[0].w : a.g;
-  const R ax = (R)(tx * gm), ay = (R)(ty * gm), az = (R)(tz * gm);
-  V4<R> an;
-  an.x = ax; an.y = ay; an.z = az; an.w = R(0);
+  V4<R> v{}, ap{}, p{};
   if (a.mode != NB_STEP_MODE_ACCEL) {
-    V4<R> v = a.vel[il];
-    if (a.mode != NB_STEP_MODE_FIRST) {  // trapezoidal kick, kernels/__init__.py:223-227
-      const V4<R> ap = a.acc[il];
-      v.x = add_rn(v.x, mul_rn(sub_rn(ax, ap.x), a.f));
-      v.y = add_rn(v.y, mul_rn(sub_rn(ay, ap.y), a.f));
-      v.z = add_rn(v.z, mul_rn(sub_rn(az, ap.z), a.f));
-    }
-    if (a.mode != NB_STEP_MODE_FINAL) {  // kick-drift, _accel_cy.pyx:218-226
-      const int64_t ig = a.i_begin + il;
-      V4<R> p = ld4_cg(a.pos + ig);
-      const R dvx = mul_rn(ax, a.dt), dvy = mul_rn(ay, a.dt), dvz = mul_rn(az, a.dt);
-      p.x = add_rn(p.x, mul_rn(add_rn(v.x, mul_rn(a.half, dvx)), a.dt));
-      p.y = add_rn(p.y, mul_rn(add_rn(v.y, mul_rn(a.half, dvy)), a.dt));
-      p.z = add_rn(p.z, mul_rn(add_rn(v.z, mul_rn(a.half, dvz)), a.dt));
-      NB_DCHECK(ig >= 0 && ig < a.n_all && il >= 0 && il < a.n_i);
-      st4(a.pos_next + ig, p);
-      for (int q = 0; q < a.n_peers; ++q) st4(a.peers[q] + ig, p);  // NVLink peer stores
-      v.x = add_rn(v.x, dvx);
-      v.y = add_rn(v.y, dvy);
-      v.z = add_rn(v.z, dvz);
-    }
-    st4(a.vel + il, v);
+    v = a.vel[il];
+    if (a.mode != NB_STEP_MODE_FIRST) ap = a.acc[il];
+    if (a.mode != NB_STEP_MODE_FINAL) p = ld4_cg(a.pos + a.i_begin + il);
   }
-  st4(a.acc + il, an);
+  integrate_body<R>(a, il, tx, ty, tz, v, ap, p);
 }
 
 // ---------------------------------------------------------------- stream-K kernel
@@ -884,8 +898,9 @@ __global__ void __launch_bounds__(T, MINB) simulate_kernel(StepArgs<typename Cor
 // over the 8 warps -- no global partials, no fixup, bitwise reproducible.  Each
 // step stages all N bodies into shared memory split-major (split s holds
 // j = s, s+S, ... contiguously, padded so a warp's lane groups read disjoint
-// banks), then one grid barrier.  Same Core arithmetic as the main kernel (the
-// FP32 split is <= N/S terms in FP32 before the FP64 sums).
+// banks), then one grid barrier per step (per-CTA release/acquire flags in its
+// place measured slower beyond ~32 CTAs: every CTA polls every flag).  Same Core arithmetic as the main kernel (the FP32 split is
+// <= N/S terms in FP32 before the FP64 sums).
 constexpr int SN_T = 256;  // threads per CTA (8 warps)
 
 // Bodies per split in shared memory: ceil(N/S) rounded up to 1 mod 8, so the
@@ -938,6 +953,11 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
       core.selfj[k] = (i < n && (int)(i % S) == s) ? (int)(i / S) : -1;
     }
   }
+  // The epilogue thread of body il keeps its velocity and previous acceleration
+  // in registers for the whole launch (it is the only one that updates them).
+  const int64_t il = blockIdx.x * (int64_t)TB + tid;
+  B vel{}, acc_prev{};
+  if (tid < TB && il < n) vel = a.vel[il];
   for (int64_t st = 0; st <= steps; ++st) {
     a.mode = st == 0 ? NB_STEP_MODE_FIRST : (st < steps ? NB_STEP_MODE_KICK_DRIFT : NB_STEP_MODE_FINAL);
     a.pos = (st & 1) ? pos_b : pos_a;
@@ -986,16 +1006,15 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
       }
     }
     __syncthreads();
-    if (tid < TB) {
-      const int64_t il = blockIdx.x * (int64_t)TB + tid;
+    if (tid < TB && il < n) {
       double t[3] = {0.0, 0.0, 0.0};
 #pragma unroll
       for (int w = 0; w < SN_T / 32; ++w)
 #pragma unroll
         for (int d = 0; d < 3; ++d) t[d] += red[(w * TB + tid) * 3 + d];
-      if (il < n) finalize_body<R>(a, il, t[0], t[1], t[2]);
+      integrate_body<R>(a, il, t[0], t[1], t[2], vel, acc_prev, sp[slot(il)]);
     }
-    grid.sync();  // new positions visible; nobody still reads the old buffer or red
+    if (st < steps) grid.sync();  // new positions visible; nobody still reads the old buffer, sp or red
   }
 }
 
