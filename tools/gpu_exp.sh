@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python tools/small_n_bench.py 10 > gpurun_out/small_n.md 2>&1
-timeout 300 python bench.py --config C1 > gpurun_out/bench_C1.json 2> gpurun_out/bench_C1.err
+NB_VARIANTS=base,old,base,old timeout 900 python tools/variants.py run C3-f32 C2 C3-f64 > gpurun_out/var_ab.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_a.json 2>&1
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_b.json 2>&1

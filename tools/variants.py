@@ -15,6 +15,7 @@ OUT = os.path.join(HERE, "variants")
 VARIANTS = {
     "base": {},
     "trace": {"NB_TRACE": 1},  # per-CTA timelines for tools/trace_launches.py
+    "old": None,  # a prebuilt library copied to tools/variants/lib_old.so (A/B against an earlier commit)
     # e^2 term of the FP64 rsqrt corrections on the FP32/INT pipes (sq_term_f32)
     "f64_mixed": {"NB_F64_MIXED": 1, "NB_DIAG_MIXED": 1},
     # i-block geometry vs N: K=4 (IB=1024: C2 = 16 whole blocks)
@@ -87,7 +88,7 @@ def build_one(name, defs):
 
 def build():
     with ThreadPoolExecutor(8) as ex:
-        for name, info in ex.map(lambda kv: build_one(*kv), VARIANTS.items()):
+        for name, info in ex.map(lambda kv: build_one(*kv), [kv for kv in VARIANTS.items() if kv[1] is not None]):
             print(f"{name:16s} {info}")
 
 
