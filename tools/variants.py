@@ -18,6 +18,20 @@ VARIANTS = {
     "old": None,  # a prebuilt library copied to tools/variants/lib_old.so (A/B against an earlier commit)
     # e^2 term of the FP64 rsqrt corrections on the FP32/INT pipes (sq_term_f32)
     "f64_mixed": {"NB_F64_MIXED": 1, "NB_DIAG_MIXED": 1},
+    # 12 / 16 warps per SM (3 / 4 per scheduler) with fewer targets per thread, same 1536-body
+    # i-block for T=384 x K=4; FP64 sums in registers to fit the 48 KB static shared memory
+    "t384_k4": {"NB_F32_T": 384, "NB_F32_K": 4, "NB_F32_TJ": 384, "NB_F32_SUMS_IN_REGS": 1,
+                "NB_F32_EXP2_MASK": 33, "NB_F32_EXP2_PHASES": 4},
+    "t384_k4_q": {"NB_F32_T": 384, "NB_F32_K": 4, "NB_F32_TJ": 384, "NB_F32_SUMS_IN_REGS": 1,
+                  "NB_F32_EXP2_MASK": 1, "NB_F32_EXP2_PHASES": 2},
+    "t512_k2": {"NB_F32_T": 512, "NB_F32_K": 2, "NB_F32_TJ": 512, "NB_F32_SUMS_IN_REGS": 1,
+                "NB_F32_EXP2_MASK": 1, "NB_F32_EXP2_PHASES": 4},
+    "t512_k2_p3": {"NB_F32_T": 512, "NB_F32_K": 2, "NB_F32_TJ": 512, "NB_F32_SUMS_IN_REGS": 1,
+                   "NB_F32_EXP2_MASK": 1, "NB_F32_EXP2_PHASES": 3, "NB_F32_UNROLL": 12},
+    "t512_k2_u8": {"NB_F32_T": 512, "NB_F32_K": 2, "NB_F32_TJ": 512, "NB_F32_SUMS_IN_REGS": 1,
+                   "NB_F32_EXP2_MASK": 1, "NB_F32_EXP2_PHASES": 4, "NB_F32_UNROLL": 8},
+    "t512_k2_smem": {"NB_F32_T": 512, "NB_F32_K": 2, "NB_F32_TJ": 512,
+                     "NB_F32_EXP2_MASK": 1, "NB_F32_EXP2_PHASES": 4},
     # i-block geometry vs N: K=4 (IB=1024: C2 = 16 whole blocks)
     # with 1/3 of the weights on LG2/EX2 over 3 source phases (K=8 exceeds 48 KB static smem;
     # 3 phases do not divide the x16 unroll: the phase test becomes a runtime branch),
