@@ -449,6 +449,29 @@ def test_ragged_sizes(prec, n, oracle):
 
 
 @pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("g", [2.5, 6.674e-11])
+@pytest.mark.parametrize("n", [700, 5000])
+def test_gravitational_constant(prec, g, n, oracle):
+    """G != 1 (SimParams.gravitational_constant; accel_soa scales by G,
+    _accel_cy.pyx:149-152): accelerations against the oracle with the same G,
+    and a short trajectory (small-N kernel at n=700, stream-K at n=5000)."""
+    s = cube(n, 3 * n, prec)
+    eps2 = 1e-3
+    a = as_mat(accel_of(s, nb.SimParams(g, 1e-3, eps2, 1)))
+    pos = s.position_matrix()
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)),
+                                s.masses.astype(np.float64), np.arange(n), g, eps2)
+    assert nb_accel_dev(a, want) <= (F64_ACC_TOL if prec == "double" else F32_ACC_TOL)
+    # dt chosen so G*dt^2 moves bodies by a comparable amount for both G
+    dt = 1e-3 / np.sqrt(g)
+    fin = nb.simulate(s, nb.SimParams(g, dt, eps2, 3))
+    ref, _ = oracle.simulate(pos.astype(np.float64), np.stack(s.velocities, 1).astype(np.float64),
+                             s.masses.astype(np.float64), g, dt, eps2, 3, threads=oracle.host_threads())
+    dev = oracle.position_dev(fin.position_matrix(), ref)
+    assert dev <= (F64_POS_TOL if prec == "double" else 2e-5), dev
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
 @pytest.mark.parametrize("n", [2, 130, 1025, 4099])
 def test_zero_softening_excludes_self(prec, n, oracle):
     s = cube(n, 7 * n, prec)
