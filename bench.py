@@ -245,6 +245,10 @@ def run_ours(args) -> dict:
         state, peer_next, p2p_barrier = _p2p_setup(pos, vel, m, dtype, i0, ni, None)
     else:
         state = DeviceState(pos, vel, m, dtype, device=dev, i_begin=i0, n_i=ni)
+    capi_gather = None
+    if world > 1 and args.transport == "capi":  # the exchange through the library's nb_comm_* C ABI
+        from paper_2203_08263_b200.sharded import _capi_allgather
+        capi_gather = _capi_allgather(None)
     pristine_pos = state.pos_a.clone()
     pristine_vel = state.vel.clone()
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -273,6 +277,10 @@ def run_ours(args) -> dict:
 
         if p2p:
             run_sharded_p2p(state, g, dt, eps2, steps, mask, peer_next, p2p_barrier)
+            return None
+
+        if capi_gather is not None:
+            run_sharded(state, g, dt, eps2, steps, mask, capi_gather, world)
             return None
 
         def gather(full, local_rows):
@@ -469,8 +477,8 @@ def main(argv=None):
     ap.add_argument("--config", default="C3-f32",
                     choices=["C1", "C2", "C3-f32", "C3-f64", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
-                    help="N>1 position exchange: NCCL all-gather (default) or the fused peer-store epilogue")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "capi", "p2p"],
+                    help="N>1 position exchange: NCCL all-gather through torch.distributed (default), the same through the library's nb_comm_* C ABI, or the fused peer-store epilogue")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-child", nargs=3, metavar=("CONFIG", "N", "KIND"), help=argparse.SUPPRESS)

@@ -46,6 +46,8 @@ extern "C" {
 #define NB_ERR_WORKSPACE 2 /* workspace pointer null or smaller than required     */
 #define NB_ERR_NODEV 3     /* no CUDA device / not an sm_100 device               */
 #define NB_ERR_CUDA 1000   /* + cudaError_t                                       */
+#define NB_ERR_NCCL 2000   /* + ncclResult_t (nb_comm_*)                           */
+#define NB_ERR_NCCL_MISSING 4 /* libnccl.so.2 could not be loaded (nb_comm_*)      */
 
 /* Update modes of the fused force+integrate step (nb_dev_step_*).
  * The velocity-Verlet loop of kernels.simulate (kernels/__init__.py:240-252) is
@@ -261,6 +263,31 @@ int nb_dev_init_f64(int kind, uint64_t seed, int64_t n, void* pos4, void* vel4, 
 /* ---------------------------------------------------------------- misc */
 
 const char* nb_last_error(void);
+/* ---------------------------------------------------------------- exchange (NCCL) */
+
+/* The per-step position exchange of the i-sharded multi-GPU loop:
+ * after a rank's fused step wrote its rows [r*n/P, (r+1)*n/P) of the next
+ * positions, every rank needs all n.  These wrap NCCL (resolved at run time from
+ * libnccl.so.2, the copy the process already uses when there is one) for hosts
+ * that are not Python; the Python driver does the same through
+ * torch.distributed.  Communicators are opaque (ncclComm_t); not re-entrant per
+ * communicator.  Two set-ups:
+ *  - one process per GPU: rank 0 calls nb_comm_unique_id, the host distributes
+ *    the NB_COMM_ID_BYTES bytes, every rank calls nb_comm_init_rank;
+ *  - one process driving ndev GPUs: nb_comm_init_all (ncclCommInitAll).
+ * nb_comm_allgather: IN PLACE on `buf` (this rank's block is at
+ * buf + rank*bytes_per_rank, every block is bytes_per_rank), stream-ordered on
+ * `stream`; with packed float4/double4 rows, bytes_per_rank = rows * 16 / 32.
+ * nb_comm_allgather_all: the same for all ndev GPUs of one process (grouped). */
+#define NB_COMM_ID_BYTES 128
+int nb_comm_unique_id(void* id_out);
+int nb_comm_init_rank(int nranks, int rank, const void* id, void** comm_out);
+int nb_comm_init_all(int ndev, const int* devs, void** comms_out);
+int nb_comm_allgather(void* buf, size_t bytes_per_rank, void* comm, void* stream);
+int nb_comm_allgather_all(void* const* bufs, size_t bytes_per_rank, void* const* comms,
+                          void* const* streams, int ndev);
+int nb_comm_destroy(void* comm);
+
 const char* nb_version(void);
 /* Number of kernel launches this library has issued on the calling process. */
 int64_t nb_launch_count(void);

@@ -58,7 +58,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
                 sys.stderr.write(log)
     objs = [os.path.join(OBJ_, s.replace(".cu", ".o")) for s in SOURCES]
     if force or jobs or _stale(lib, objs):
-        link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs]
+        link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs, "-ldl"]
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(link)}\n{r.stdout}\n{r.stderr}")

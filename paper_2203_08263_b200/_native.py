@@ -82,6 +82,16 @@ def lib() -> ctypes.CDLL:
         L.nb_dev_workspace_bytes.restype = _i64
         L.nb_energy_workspace_bytes.argtypes = [_i, _i64]
         L.nb_energy_workspace_bytes.restype = _i64
+        L.nb_comm_unique_id.argtypes = [_p]
+        L.nb_comm_init_rank.argtypes = [_i, _i, _p, ctypes.POINTER(_p)]
+        L.nb_comm_init_all.argtypes = [_i, ctypes.POINTER(_i), ctypes.POINTER(_p)]
+        L.nb_comm_allgather.argtypes = [_p, ctypes.c_size_t, _p, _p]
+        L.nb_comm_allgather_all.argtypes = [ctypes.POINTER(_p), ctypes.c_size_t, ctypes.POINTER(_p),
+                                            ctypes.POINTER(_p), _i]
+        L.nb_comm_destroy.argtypes = [_p]
+        for f in ("nb_comm_unique_id", "nb_comm_init_rank", "nb_comm_init_all", "nb_comm_allgather",
+                  "nb_comm_allgather_all", "nb_comm_destroy"):
+            getattr(L, f).restype = _i
         L.nb_last_error.restype = ctypes.c_char_p
         L.nb_version.restype = ctypes.c_char_p
         L.nb_launch_count.restype = _i64
@@ -96,6 +106,33 @@ def call(name: str, *args) -> None:
     if rc != 0:
         msg = L.nb_last_error()
         raise NativeError(name, rc, msg.decode() if msg else "")
+
+
+COMM_ID_BYTES = 128
+
+
+def comm_unique_id() -> bytes:
+    """NB_COMM_ID_BYTES of NCCL unique id (rank 0 makes it, the host shares it)."""
+    buf = ctypes.create_string_buffer(COMM_ID_BYTES)
+    call("nb_comm_unique_id", buf)
+    return buf.raw
+
+
+def comm_init_rank(nranks: int, rank: int, uid: bytes) -> int:
+    """Opaque NCCL communicator handle for one rank (nb_comm_init_rank)."""
+    if len(uid) != COMM_ID_BYTES:
+        raise ValueError(f"unique id must be {COMM_ID_BYTES} bytes")
+    out = ctypes.c_void_p()
+    call("nb_comm_init_rank", nranks, rank, ctypes.create_string_buffer(uid, COMM_ID_BYTES), ctypes.byref(out))
+    return int(out.value)
+
+
+def comm_allgather(buf_ptr: int, bytes_per_rank: int, comm: int, stream: int) -> None:
+    call("nb_comm_allgather", buf_ptr, bytes_per_rank, comm, stream)
+
+
+def comm_destroy(comm: int) -> None:
+    call("nb_comm_destroy", comm)
 
 
 def energy_workspace_bytes(precision_bytes: int, n: int) -> int:

@@ -4,8 +4,12 @@
 // /root/reference/pkg/src/nbodybench/kernels/_accel_cy.pyx) and the step loop of
 // kernels.simulate (kernels/__init__.py:230-253) on host pointers; nb_dev_* are
 // the stream-ordered device-pointer entry points the Python host code drives.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <atomic>
 #include <cmath>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -699,6 +703,142 @@ __attribute__((visibility("default"))) int nb_trace_setup(void* buf, int64_t cap
 }
 __attribute__((visibility("default"))) int64_t nb_trace_count(void) { return nb::trace_count(); }
 #endif
+// ---------------------------------------------------------------- position exchange (NCCL)
+// The per-step exchange of SURVEY.md 8(e) behind the C ABI, for hosts that are
+// not Python (the Python driver uses torch.distributed's NCCL): communicator
+// set-up and the in-place all-gather of a rank's position rows.  NCCL is
+// resolved at run time from "libnccl.so.2" -- the copy the host process already
+// loaded (e.g. PyTorch's) when there is one -- so the library has no link-time
+// NCCL dependency and never carries a second NCCL into the process.
+namespace {
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommInitAll) comm_init_all = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclCommUserRank) comm_user_rank = nullptr;
+  decltype(&ncclCommCount) comm_count = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  std::string error;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* e = dlerror();
+      api.error = std::string("cannot load libnccl.so.2: ") + (e ? e : "unknown");
+      return;
+    }
+#define NB_NCCL_SYM(field, name)                                        \
+  api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name));     \
+  if (!api.field) { api.error = std::string("libnccl.so.2 lacks ") + name; return; }
+    NB_NCCL_SYM(get_unique_id, "ncclGetUniqueId");
+    NB_NCCL_SYM(comm_init_rank, "ncclCommInitRank");
+    NB_NCCL_SYM(comm_init_all, "ncclCommInitAll");
+    NB_NCCL_SYM(all_gather, "ncclAllGather");
+    NB_NCCL_SYM(comm_destroy, "ncclCommDestroy");
+    NB_NCCL_SYM(comm_user_rank, "ncclCommUserRank");
+    NB_NCCL_SYM(comm_count, "ncclCommCount");
+    NB_NCCL_SYM(group_start, "ncclGroupStart");
+    NB_NCCL_SYM(group_end, "ncclGroupEnd");
+    NB_NCCL_SYM(error_string, "ncclGetErrorString");
+#undef NB_NCCL_SYM
+  });
+  return api;
+}
+
+int nccl_fail(ncclResult_t r, const char* where) {
+  const NcclApi& api = nccl_api();
+  t_err = std::string(where) + ": " + (api.error_string ? api.error_string(r) : "nccl error");
+  return NB_ERR_NCCL + (int)r;
+}
+#define NB_NCCL(call)                                        \
+  do {                                                       \
+    ncclResult_t r_ = (call);                                \
+    if (r_ != ncclSuccess) return nccl_fail(r_, #call);      \
+  } while (0)
+#define NB_NCCL_API(api)                                                         \
+  const NcclApi& api = nccl_api();                                               \
+  if (!api.all_gather) return fail(NB_ERR_NCCL_MISSING, api.error)
+}  // namespace
+
+int nb_comm_unique_id(void* id_out) {
+  if (!id_out) return fail(NB_ERR_ARG, "id_out must hold NB_COMM_ID_BYTES bytes");
+  NB_NCCL_API(api);
+  ncclUniqueId id;
+  NB_NCCL(api.get_unique_id(&id));
+  std::memcpy(id_out, &id, sizeof(id));
+  return NB_OK;
+}
+
+int nb_comm_init_rank(int nranks, int rank, const void* id, void** comm_out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NB_ERR_ARG, "need 0 <= rank < nranks");
+  if (!id || !comm_out) return fail(NB_ERR_ARG, "null id or comm_out");
+  NB_NCCL_API(api);
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclComm_t c = nullptr;
+  NB_NCCL(api.comm_init_rank(&c, nranks, uid, rank));
+  *comm_out = c;
+  return NB_OK;
+}
+
+int nb_comm_init_all(int ndev, const int* devs, void** comms_out) {
+  if (ndev < 1 || !comms_out) return fail(NB_ERR_ARG, "need ndev >= 1 and comms_out[ndev]");
+  NB_NCCL_API(api);
+  std::vector<ncclComm_t> c((size_t)ndev, nullptr);
+  NB_NCCL(api.comm_init_all(c.data(), ndev, devs));
+  for (int q = 0; q < ndev; ++q) comms_out[q] = c[q];
+  return NB_OK;
+}
+
+int nb_comm_allgather(void* buf, size_t bytes_per_rank, void* comm, void* stream) {
+  if (!buf || !comm) return fail(NB_ERR_ARG, "null buffer or communicator");
+  NB_NCCL_API(api);
+  int rank = 0;
+  NB_NCCL(api.comm_user_rank(static_cast<ncclComm_t>(comm), &rank));
+  char* b = static_cast<char*>(buf);
+  NB_NCCL(api.all_gather(b + (size_t)rank * bytes_per_rank, b, bytes_per_rank, ncclChar,
+                         static_cast<ncclComm_t>(comm), static_cast<cudaStream_t>(stream)));
+  return NB_OK;
+}
+
+int nb_comm_allgather_all(void* const* bufs, size_t bytes_per_rank, void* const* comms, void* const* streams,
+                          int ndev) {
+  if (ndev < 1 || !bufs || !comms || !streams) return fail(NB_ERR_ARG, "need ndev >= 1 and bufs/comms/streams");
+  NB_NCCL_API(api);
+  NB_NCCL(api.group_start());
+  for (int q = 0; q < ndev; ++q) {
+    int rank = 0;
+    ncclResult_t r = api.comm_user_rank(static_cast<ncclComm_t>(comms[q]), &rank);
+    if (r == ncclSuccess) {
+      char* b = static_cast<char*>(bufs[q]);
+      r = api.all_gather(b + (size_t)rank * bytes_per_rank, b, bytes_per_rank, ncclChar,
+                         static_cast<ncclComm_t>(comms[q]), static_cast<cudaStream_t>(streams[q]));
+    }
+    if (r != ncclSuccess) {
+      api.group_end();
+      return nccl_fail(r, "ncclAllGather");
+    }
+  }
+  NB_NCCL(api.group_end());
+  return NB_OK;
+}
+
+int nb_comm_destroy(void* comm) {
+  if (!comm) return NB_OK;
+  NB_NCCL_API(api);
+  NB_NCCL(api.comm_destroy(static_cast<ncclComm_t>(comm)));
+  return NB_OK;
+}
+
 const char* nb_version(void) { return "nbody_b200 0.1.0 (sm_100a)"; }
 int64_t nb_launch_count(void) { return g_launches.load(); }
 

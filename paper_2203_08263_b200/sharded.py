@@ -139,6 +139,53 @@ def _torch_allgather(group):
     return gather
 
 
+_COMM_CACHE: dict = {}
+
+
+class _StreamWait:
+    """Handle of an exchange running on a side stream: wait() orders the current
+    (compute) stream after it."""
+
+    def __init__(self, event):
+        self.event = event
+
+    def wait(self) -> None:
+        import torch
+        torch.cuda.current_stream().wait_event(self.event)
+
+
+def _capi_allgather(group):
+    """The exchange through the library's own C ABI (nb_comm_*), as a host that
+    is not Python would drive it: rank 0's NCCL unique id is shared over the
+    process group, every rank opens its communicator with nb_comm_init_rank
+    (cached per group), and each gather is nb_comm_allgather in place on a side
+    stream that starts after the drift step and is waited on before the remote-
+    source pass -- the same overlap as the torch.distributed transport."""
+    import torch
+    import torch.distributed as dist
+
+    from . import _native
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    key = (id(group), world, rank, torch.cuda.current_device())
+    entry = _COMM_CACHE.get(key)
+    if entry is None:
+        box = [_native.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        entry = _COMM_CACHE[key] = (_native.comm_init_rank(world, rank, box[0]), torch.cuda.Stream())
+    comm, side = entry
+
+    def gather(full, local):
+        ready = torch.cuda.Event()
+        ready.record()
+        side.wait_event(ready)
+        _native.comm_allgather(full.data_ptr(), local.numel() * local.element_size(), comm, side.cuda_stream)
+        done = torch.cuda.Event()
+        done.record(side)
+        return _StreamWait(done)
+    return gather
+
+
 def _p2p_setup(pos, vel, m, dtype, i0, ni, group):
     """Positions in symmetric memory (CUDA IPC-mapped on every peer) and the
     symmetric-memory device barrier."""
@@ -199,7 +246,8 @@ def simulate_sharded(positions: np.ndarray, velocities: np.ndarray, masses: np.n
     """Multi-GPU simulate: every rank passes the full initial state and gets the
     full final (positions, velocities) back.  Uses the default process group
     (NCCL, one process per GPU) unless ``group`` is given.  ``transport``:
-    "nccl" (in-place all-gather overlapped with the local-source pass) or "p2p"
+    "nccl" (in-place all-gather overlapped with the local-source pass), "capi"
+    (the same exchange through the library's nb_comm_* C ABI) or "p2p"
     (peer-store epilogue into symmetric-memory buffers; see run_sharded_p2p)."""
     import torch
     import torch.distributed as dist
@@ -221,11 +269,12 @@ def simulate_sharded(positions: np.ndarray, velocities: np.ndarray, masses: np.n
     if transport == "p2p":
         state, peer_next, barrier = _p2p_setup(pos, vel, m, dtype, i0, ni, group)
         run_sharded_p2p(state, g, dt, eps2, steps, flags, peer_next, barrier)
-    elif transport == "nccl":
+    elif transport in ("nccl", "capi"):
         state = _shard_state(pos, vel, m, dtype, i0, ni)
-        run_sharded(state, g, dt, eps2, steps, flags, _torch_allgather(group), world)
+        gather = _torch_allgather(group) if transport == "nccl" else _capi_allgather(group)
+        run_sharded(state, g, dt, eps2, steps, flags, gather, world)
     else:
-        raise ValueError(f"unknown transport {transport!r} (expected 'nccl' or 'p2p')")
+        raise ValueError(f"unknown transport {transport!r} (expected 'nccl', 'capi' or 'p2p')")
     vel_full = torch.empty((npad, 4), dtype=state.vel.dtype, device=state.device)
     gather_into(vel_full, state.vel[:ni].contiguous(), group)
     out_pos = state.pos_cur[:n, :3].cpu().numpy()

@@ -53,6 +53,16 @@ def test_argument_errors_without_device(lib):
     # n_i == 0 is a no-op, not an error
     _native.call("nb_dev_step_f32", None, 10, 0, 0, 0, 10, 1.0, 0.0, 0.0, 0, 0, None, 0,
                  None, None, None, None, 0, None)
+    # the exchange ABI validates before it loads NCCL
+    with pytest.raises(_native.NativeError) as e:
+        _native.comm_init_rank(0, 0, bytes(_native.COMM_ID_BYTES))
+    assert e.value.code == 1 and "rank" in str(e.value)
+    with pytest.raises(_native.NativeError) as e:
+        _native.comm_allgather(0, 64, 0, 0)
+    assert e.value.code == 1
+    with pytest.raises(ValueError):
+        _native.comm_init_rank(2, 0, b"short")
+    _native.comm_destroy(0)  # null communicator: no-op
 
 
 def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):

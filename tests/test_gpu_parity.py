@@ -421,6 +421,32 @@ def test_small_simulate_kernel(prec, n, eps2, uniform, oracle, monkeypatch):
         assert d_path <= max(2e-5, 2 * d_sk)
 
 
+def test_exchange_c_abi_single_gpu():
+    """nb_comm_* (the NCCL position exchange behind the C ABI) on the one GPU
+    this run has: unique id -> a 1-rank communicator -> in-place all-gather of
+    packed rows (nothing to receive: the buffer is unchanged) -> destroy; and
+    the single-process set-up (ncclCommInitAll) with its grouped all-gather."""
+    import ctypes
+    import torch
+    t = torch.arange(64 * 4, dtype=torch.float32, device="cuda").reshape(64, 4)
+    want = t.clone()
+    stream = torch.cuda.current_stream().cuda_stream
+    comm = _native.comm_init_rank(1, 0, _native.comm_unique_id())
+    _native.comm_allgather(t.data_ptr(), t.numel() * 4, comm, stream)
+    torch.cuda.synchronize()
+    assert torch.equal(t, want)
+    _native.comm_destroy(comm)
+    comms = (ctypes.c_void_p * 1)()
+    devs = (ctypes.c_int * 1)(torch.cuda.current_device())
+    _native.call("nb_comm_init_all", 1, devs, comms)
+    bufs = (ctypes.c_void_p * 1)(t.data_ptr())
+    streams = (ctypes.c_void_p * 1)(stream)
+    _native.call("nb_comm_allgather_all", bufs, t.numel() * 4, comms, streams, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(t, want)
+    _native.comm_destroy(comms[0])
+
+
 def test_native_kernels_launched():
     before = _native.launch_count()
     nb.simulate(cube(64, 1, "single"), nb.SimParams(1.0, 1e-3, 1e-3, 2))
