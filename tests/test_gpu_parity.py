@@ -447,6 +447,21 @@ def test_exchange_c_abi_single_gpu():
     _native.comm_destroy(comms[0])
 
 
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("n", [2560, 2561, 4096, 4097, 8192, 8193])
+def test_simulate_path_boundaries(prec, n, oracle):
+    """simulate() switches kernels with N (small-N cooperative kernel up to
+    4096 FP32 / 2560 FP64, stream-K persistent kernel up to 8192, per-step
+    launches beyond): trajectories on both sides of each switch agree with the
+    FP64 oracle."""
+    s = cube(n, 11, prec)
+    fin = nb.simulate(s, nb.SimParams(1.0, 1e-3, 1e-3, 3))
+    ref, _ = oracle.simulate(s.position_matrix().astype(np.float64), np.stack(s.velocities, 1).astype(np.float64),
+                             s.masses.astype(np.float64), 1.0, 1e-3, 1e-3, 3, threads=oracle.host_threads())
+    dev = oracle.position_dev(fin.position_matrix(), ref)
+    assert dev <= (F64_POS_TOL if prec == "double" else 2e-5), dev
+
+
 def test_native_kernels_launched():
     before = _native.launch_count()
     nb.simulate(cube(64, 1, "single"), nb.SimParams(1.0, 1e-3, 1e-3, 2))
