@@ -644,6 +644,27 @@ def test_full_size_trajectory_properties():
     assert np.linalg.norm(p1 - p0) <= 1e-5 * scale
 
 
+@pytest.mark.parametrize("config", ["C3-f32", "C4"])
+def test_full_size_energy_conservation(config):
+    """BASELINE sizes (C3-f32 N=131072, C4 N=524288 FP64): total energy from the
+    FP64 diagnostics pass drifts by at most 1e-4 relative (the reference's
+    acceptance bound, pkg/tests/test_acceptance.py:80-86, here at full size where
+    the reference's O(N^2) Python diagnostics cannot run).  The BASELINE dt
+    (1e-3) does not resolve these systems' collapse -- |a| ~ N/R^2 ~ 1e5, the
+    dynamical time ~3e-3 -- so energy is not conserved at that dt on any
+    implementation; the check runs the same states with dt = 1e-6."""
+    cfg = nb.BASELINE_CONFIGS[config]
+    s = cfg.system()
+    p = nb.SimParams(1.0, 1e-6, cfg.softening_sq, 10)
+    e0 = nb.diagnostics_gpu(s, p)
+    fin = nb.simulate(s, p)
+    e1 = nb.diagnostics_gpu(fin, p)
+    drift = abs(e1["total"] - e0["total"]) / abs(e0["total"])
+    print(f"{config}: E0 {e0['total']:.12e} E1 {e1['total']:.12e} drift {drift:.3e}")
+    # measured 2.5e-10 (C3-f32) and 1.6e-12 (C4): assert 100x inside the reference bound
+    assert np.isfinite(e1["total"]) and drift <= 1e-6
+
+
 # --------------------------------------------------------------------------- sharding on one GPU
 
 @pytest.mark.parametrize("prec", ["double", "single"])
