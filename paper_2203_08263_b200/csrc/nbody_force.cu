@@ -38,6 +38,7 @@
 
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <mutex>
 
 // Tuning knobs (overridable with -D for variant sweeps, tools/variants.py).
 #ifndef NB_F32_K
@@ -1099,6 +1100,8 @@ static int grid_for(const void* fn, int threads) {
   struct Entry { int dev; const void* fn; int grid; };
   static Entry cache[64];
   static int used = 0;
+  static std::mutex mu;  // host threads may launch concurrently on different streams
+  std::lock_guard<std::mutex> lock(mu);
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   for (int k = 0; k < used; ++k)
@@ -1249,6 +1252,8 @@ cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>*
   static Cap caps[64];
   static Opt opts[32];
   static int n_caps = 0, n_opts = 0;
+  static std::mutex mu;  // host threads may launch concurrently on different streams
+  std::unique_lock<std::mutex> lock(mu);
   int dev = 0;
   cudaGetDevice(&dev);
   Opt* opt = nullptr;
@@ -1273,6 +1278,7 @@ cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>*
     capacity = per_sm * sms;
     if (n_caps < 64) caps[n_caps++] = Cap{dev, fn, smem, capacity};
   }
+  lock.unlock();
   const int64_t grid = (n + 2 * ppw - 1) / (2 * ppw);
   if (grid > (int64_t)capacity) return cudaErrorCooperativeLaunchTooLarge;
   int64_t L = small_split_stride(n, (SN_T / 32) * (32 / ppw));
