@@ -24,6 +24,10 @@ VARIANTS = {
                 "NB_F32_EXP2_MASK": 33, "NB_F32_EXP2_PHASES": 4},
     "t384_k4_q": {"NB_F32_T": 384, "NB_F32_K": 4, "NB_F32_TJ": 384, "NB_F32_SUMS_IN_REGS": 1,
                   "NB_F32_EXP2_MASK": 1, "NB_F32_EXP2_PHASES": 2},
+    # 8 targets per thread (more independent chains per warp) in 128-thread CTAs, 2 per SM
+    "t128_k8_b2": {"NB_F32_T": 128, "NB_F32_K": 8, "NB_F32_MINB": 2, "NB_F32_EXP2_MASK": 37},
+    "t128_k8_b2_q": {"NB_F32_T": 128, "NB_F32_K": 8, "NB_F32_MINB": 2, "NB_F32_EXP2_MASK": 33},
+    "t128_k8_b1": {"NB_F32_T": 128, "NB_F32_K": 8, "NB_F32_MINB": 1, "NB_F32_EXP2_MASK": 37},
     "t512_k2": {"NB_F32_T": 512, "NB_F32_K": 2, "NB_F32_TJ": 512, "NB_F32_SUMS_IN_REGS": 1,
                 "NB_F32_EXP2_MASK": 1, "NB_F32_EXP2_PHASES": 4},
     "t512_k2_p3": {"NB_F32_T": 512, "NB_F32_K": 2, "NB_F32_TJ": 512, "NB_F32_SUMS_IN_REGS": 1,
