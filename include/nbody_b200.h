@@ -205,6 +205,25 @@ int nb_dev_pack_f64(const void* x, const void* y, const void* z, const void* w, 
 int nb_dev_unpack_f32(const void* in4, int64_t n, void* x, void* y, void* z, void* stream);
 int nb_dev_unpack_f64(const void* in4, int64_t n, void* x, void* y, void* z, void* stream);
 
+/* SURVEY 8(b)'s proposed minimal pair, for hosts that schedule the force pass and
+ * the update separately (the product path fuses them in nb_dev_step_* /
+ * nb_dev_simulate_*):
+ * nb_force: acc_out[k] = G * sum_j m_j d / (|d|^2 + eps2)^(3/2) for the targets
+ *   [i_begin, i_begin+n_i) of pos_all against all n_all sources (the self pair is
+ *   excluded explicitly when (real)eps2 == 0); workspace as for nb_dev_step_*.
+ * nb_update: the step update of one shard's n_i rows with the reference's
+ *   rounding (mode NB_STEP_FIRST / NB_STEP_KICK_DRIFT / NB_STEP_FINAL_KICK, as in
+ *   the fused step): pos_next = drifted pos_cur (= pos_cur for the final kick),
+ *   vel updated in place; acc_prev is read by the kick modes only. */
+int nb_force_f32(const void* pos_all, int64_t n_all, int64_t i_begin, int64_t n_i, double eps2,
+                 double g, void* acc_out, void* workspace, int64_t workspace_bytes, void* stream);
+int nb_force_f64(const void* pos_all, int64_t n_all, int64_t i_begin, int64_t n_i, double eps2,
+                 double g, void* acc_out, void* workspace, int64_t workspace_bytes, void* stream);
+int nb_update_f32(void* pos_next, const void* pos_cur, void* vel, const void* acc,
+                  const void* acc_prev, int64_t n_i, double dt, int mode, void* stream);
+int nb_update_f64(void* pos_next, const void* pos_cur, void* vel, const void* acc,
+                  const void* acc_prev, int64_t n_i, double dt, int mode, void* stream);
+
 /* The same conversion fused with its transfer, for simulate()'s column staging:
  * one call each way (small N is host-latency-bound).  Column block layout, in
  * elements of the system precision: x, y, z, m of all n bodies at 0, n, 2n, 3n,

@@ -46,6 +46,8 @@ _ARGTYPES = {
                               ctypes.POINTER(ctypes.c_float)],
     "nb_dev_pack": [_p, _p, _p, _p, _i64, _p, _p],
     "nb_dev_unpack": [_p, _i64, _p, _p, _p, _p],
+    "nb_force": [_p, _i64, _i64, _i64, _d, _d, _p, _p, _i64, _p],
+    "nb_update": [_p, _p, _p, _p, _p, _i64, _d, _i, _p],
     "nb_dev_load_cols": [_p, _p, _i64, _i64, _p, _p, _p],
     "nb_dev_store_cols": [_p, _p, _i64, _i64, _p, _p, _p],
     "nb_dev_drift": [_p, _p, _p, _i64, _d, _p],

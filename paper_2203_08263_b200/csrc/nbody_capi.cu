@@ -426,6 +426,32 @@ int dev_unpack(const void* in4, int64_t n, void* x, void* y, void* z, void* stre
   return NB_OK;
 }
 
+// SURVEY.md 8(b)'s proposed minimal surface: the force pass alone and the update
+// alone (the product path fuses them; these serve hosts that schedule the two).
+template <typename R>
+int dev_force(const void* pos_all, int64_t n_all, int64_t i_begin, int64_t n_i, double eps2, double g,
+              void* acc_out, void* workspace, int64_t workspace_bytes, void* stream) {
+  const int flags = eps2 > 0.0 && (R)eps2 > (R)0 ? 0 : NB_FLAG_EXCLUDE_SELF;
+  return dev_step<R>(pos_all, n_all, i_begin, n_i, 0, n_all, g, eps2, 0.0, NB_MODE_ACCEL, flags, nullptr, 0,
+                     acc_out, nullptr, nullptr, workspace, workspace_bytes, stream);
+}
+
+template <typename R>
+int dev_update(void* pos_next, const void* pos_cur, void* vel, const void* acc, const void* acc_prev, int64_t n_i,
+               double dt, int mode, void* stream) {
+  if (n_i < 0) return fail(NB_ERR_ARG, "n_i must be >= 0");
+  if (mode < NB_STEP_FIRST || mode > NB_STEP_FINAL_KICK) return fail(NB_ERR_ARG, "mode must be an NB_STEP_* mode");
+  if (!(dt > 0.0)) return fail(NB_ERR_ARG, "dt must be positive");
+  if (n_i == 0) return NB_OK;
+  if (!pos_next || !pos_cur || !vel || !acc || (mode != NB_STEP_FIRST && !acc_prev))
+    return fail(NB_ERR_ARG, "null device pointer");
+  if (cudaError_t be = bind_device_of(vel)) return cuda_fail(be, "vel4 is not a device pointer");
+  NB_CUDA(launch_update<R>(static_cast<V4<R>*>(pos_next), static_cast<const V4<R>*>(pos_cur),
+                           static_cast<V4<R>*>(vel), static_cast<const V4<R>*>(acc),
+                           static_cast<const V4<R>*>(acc_prev), n_i, dt, mode, static_cast<cudaStream_t>(stream)));
+  return NB_OK;
+}
+
 // Column block of simulate()'s staging (header: nb_dev_load_cols_*).
 template <typename R>
 int dev_load_cols(const void* host_cols, void* dev_cols, int64_t n, int64_t n_i, void* pos4, void* vel4,
@@ -637,6 +663,22 @@ int nb_dev_unpack_f32(const void* in4, int64_t n, void* x, void* y, void* z, voi
 }
 int nb_dev_unpack_f64(const void* in4, int64_t n, void* x, void* y, void* z, void* stream) {
   return dev_unpack<double>(in4, n, x, y, z, stream);
+}
+int nb_force_f32(const void* pos_all, int64_t n_all, int64_t i_begin, int64_t n_i, double eps2, double g,
+                 void* acc_out, void* workspace, int64_t workspace_bytes, void* stream) {
+  return dev_force<float>(pos_all, n_all, i_begin, n_i, eps2, g, acc_out, workspace, workspace_bytes, stream);
+}
+int nb_force_f64(const void* pos_all, int64_t n_all, int64_t i_begin, int64_t n_i, double eps2, double g,
+                 void* acc_out, void* workspace, int64_t workspace_bytes, void* stream) {
+  return dev_force<double>(pos_all, n_all, i_begin, n_i, eps2, g, acc_out, workspace, workspace_bytes, stream);
+}
+int nb_update_f32(void* pos_next, const void* pos_cur, void* vel, const void* acc, const void* acc_prev,
+                  int64_t n_i, double dt, int mode, void* stream) {
+  return dev_update<float>(pos_next, pos_cur, vel, acc, acc_prev, n_i, dt, mode, stream);
+}
+int nb_update_f64(void* pos_next, const void* pos_cur, void* vel, const void* acc, const void* acc_prev,
+                  int64_t n_i, double dt, int mode, void* stream) {
+  return dev_update<double>(pos_next, pos_cur, vel, acc, acc_prev, n_i, dt, mode, stream);
 }
 int nb_dev_load_cols_f32(const void* host_cols, void* dev_cols, int64_t n, int64_t n_i, void* pos4, void* vel4,
                          void* stream) {

@@ -61,6 +61,8 @@ inline int64_t counters_bytes(int64_t n_iblocks) { return ((n_iblocks * 4 + 255)
 
 // Stand-alone O(N) kernels (nbody_update.cu).
 template <typename R> cudaError_t launch_drift(V4<R>* pos, V4<R>* vel, const V4<R>* acc, int64_t n, double dt, cudaStream_t s);
+template <typename R> cudaError_t launch_update(V4<R>* pos_next, const V4<R>* pos_cur, V4<R>* vel, const V4<R>* acc,
+                                                const V4<R>* acc_prev, int64_t n, double dt, int mode, cudaStream_t s);
 template <typename R> cudaError_t launch_kick(V4<R>* vel, const V4<R>* an, const V4<R>* ao, int64_t n, double factor, cudaStream_t s);
 template <typename R> cudaError_t launch_pack_soa(const R* x, const R* y, const R* z, const R* w, V4<R>* out, int64_t n, cudaStream_t s);
 template <typename R> cudaError_t launch_unpack_soa(const V4<R>* in, R* x, R* y, R* z, int64_t n, cudaStream_t s);

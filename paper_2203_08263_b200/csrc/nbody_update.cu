@@ -209,6 +209,47 @@ __global__ void __launch_bounds__(256) energy_final_kernel(const double* part, i
 }
 
 // ---------------------------------------------------------------- launchers
+// The step update of the fused epilogue as a stand-alone pass (nb_update_*):
+// mode FIRST: dv = a dt; p' = p + (v + half dv) dt; v += dv; KICK_DRIFT: first
+// v += (a - a_prev) f with f = real(0.5 dt) (kernels/__init__.py:223-227), then
+// FIRST; FINAL: the kick only (p' = p).  Same rounding sequence as the epilogue.
+template <typename R>
+__global__ void update_kernel(V4<R>* pos_next, const V4<R>* pos_cur, V4<R>* vel, const V4<R>* acc,
+                              const V4<R>* acc_prev, int64_t n, R dt, R f, int mode) {
+  const R half = R(0.5);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    V4<R> p = pos_cur[i], v = vel[i];
+    const V4<R> a = acc[i];
+    if (mode != NB_STEP_MODE_FIRST) {
+      const V4<R> ap = acc_prev[i];
+      v.x = add_rn(v.x, mul_rn(sub_rn(a.x, ap.x), f));
+      v.y = add_rn(v.y, mul_rn(sub_rn(a.y, ap.y), f));
+      v.z = add_rn(v.z, mul_rn(sub_rn(a.z, ap.z), f));
+    }
+    if (mode != NB_STEP_MODE_FINAL) {
+      const R dvx = mul_rn(a.x, dt), dvy = mul_rn(a.y, dt), dvz = mul_rn(a.z, dt);
+      p.x = add_rn(p.x, mul_rn(add_rn(v.x, mul_rn(half, dvx)), dt));
+      p.y = add_rn(p.y, mul_rn(add_rn(v.y, mul_rn(half, dvy)), dt));
+      p.z = add_rn(p.z, mul_rn(add_rn(v.z, mul_rn(half, dvz)), dt));
+      v.x = add_rn(v.x, dvx);
+      v.y = add_rn(v.y, dvy);
+      v.z = add_rn(v.z, dvz);
+    }
+    st4(pos_next + i, p);
+    st4(vel + i, v);
+  }
+}
+
+template <typename R>
+cudaError_t launch_update(V4<R>* pos_next, const V4<R>* pos_cur, V4<R>* vel, const V4<R>* acc,
+                          const V4<R>* acc_prev, int64_t n, double dt, int mode, cudaStream_t s) {
+  update_kernel<R><<<blocks_for(n, 256), 256, 0, s>>>(pos_next, pos_cur, vel, acc, acc_prev, n, (R)dt,
+                                                       (R)(0.5 * dt), mode);
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <typename R>
 cudaError_t launch_drift(V4<R>* pos, V4<R>* vel, const V4<R>* acc, int64_t n, double dt, cudaStream_t s) {
   drift_kernel<R><<<blocks_for(n, 256), 256, 0, s>>>(pos, vel, acc, n, (R)dt);
@@ -301,6 +342,8 @@ cudaError_t launch_energy(const V4<R>* pos, const V4<R>* vel, int64_t n, double 
 
 #define NB_INST(R)                                                                                  \
   template cudaError_t launch_drift<R>(V4<R>*, V4<R>*, const V4<R>*, int64_t, double, cudaStream_t); \
+  template cudaError_t launch_update<R>(V4<R>*, const V4<R>*, V4<R>*, const V4<R>*, const V4<R>*, int64_t,  \
+                                        double, int, cudaStream_t);                                        \
   template cudaError_t launch_kick<R>(V4<R>*, const V4<R>*, const V4<R>*, int64_t, double, cudaStream_t); \
   template cudaError_t launch_pack_soa<R>(const R*, const R*, const R*, const R*, V4<R>*, int64_t, cudaStream_t); \
   template cudaError_t launch_unpack_soa<R>(const V4<R>*, R*, R*, R*, int64_t, cudaStream_t);       \

@@ -462,6 +462,45 @@ def test_simulate_path_boundaries(prec, n, oracle):
     assert dev <= (F64_POS_TOL if prec == "double" else 2e-5), dev
 
 
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("eps2", [1e-3, 0.0])
+def test_separate_force_and_update_match_fused(prec, eps2, monkeypatch):
+    """SURVEY 8(b)'s proposed pair: nb_force then nb_update each step (two acc
+    buffers, the host schedules the modes) equals the fused per-step path of
+    nb_dev_simulate bit for bit -- same force decomposition, same rounding
+    sequence in the update."""
+    import torch
+    from paper_2203_08263_b200.device import DeviceState, kernel_flags
+    from paper_2203_08263_b200._native import NB_STEP_FIRST, NB_STEP_KICK_DRIFT, NB_STEP_FINAL_KICK
+    monkeypatch.setenv("NB_SMALL_MAX_N", "0")
+    monkeypatch.setenv("NB_PERSISTENT_MAX_N", "0")
+    n, steps, dt = 3000, 4, 1e-3
+    s = cube(n, 17, prec)
+    dtype = s.precision.dtype
+    pos, vel = s.position_matrix().astype(dtype), np.stack(s.velocities, 1)
+    fused = DeviceState(pos, vel, s.masses, dtype)
+    fused.simulate(1.0, dt, eps2, steps, kernel_flags(s.masses, eps2, dtype))
+    st = DeviceState(pos, vel, s.masses, dtype)
+    sfx = st.sfx
+    stream = torch.cuda.current_stream().cuda_stream
+    acc = [torch.zeros_like(st.acc), torch.zeros_like(st.acc)]
+    cur, nxt = st.pos_a, st.pos_b
+    for k in range(steps + 1):
+        mode = NB_STEP_FIRST if k == 0 else (NB_STEP_KICK_DRIFT if k < steps else NB_STEP_FINAL_KICK)
+        a_new, a_old = acc[k % 2], acc[(k + 1) % 2]
+        _native.call("nb_force" + sfx, cur.data_ptr(), n, 0, n, eps2, 1.0, a_new.data_ptr(), st.ws.data_ptr(),
+                     st.ws_bytes, stream)
+        _native.call("nb_update" + sfx, nxt.data_ptr(), cur.data_ptr(), st.vel.data_ptr(), a_new.data_ptr(),
+                     a_old.data_ptr(), n, dt, mode, stream)
+        if mode != NB_STEP_FINAL_KICK:
+            cur, nxt = nxt, cur
+    torch.cuda.synchronize()
+    # the final kick writes pos_next = pos_cur: compare the state the fused path reports
+    np.testing.assert_array_equal(cur[:, :3].cpu().numpy(), fused.positions_host())
+    np.testing.assert_array_equal(st.vel[:, :3].cpu().numpy(), fused.velocities_host())
+    np.testing.assert_array_equal(acc[steps % 2][:, :3].cpu().numpy(), fused.acc[:, :3].cpu().numpy())
+
+
 def test_native_kernels_launched():
     before = _native.launch_count()
     nb.simulate(cube(64, 1, "single"), nb.SimParams(1.0, 1e-3, 1e-3, 2))
