@@ -147,8 +147,18 @@ int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int6
                              carry_mode, acc4, vel4, pos4_next, workspace, workspace_bytes, stream, peers, n_peers);
   if (rc == -1) return NB_OK;
   if (rc) return rc;
-  cudaError_t e = launch_step<R>(a, flags & (NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS),
-                                 static_cast<cudaStream_t>(stream));
+  const int kf = flags & (NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS);
+  if (mode == NB_MODE_ACCEL && carry_mode == 0 && n_peers == 0 && i_begin == 0 && n_i == n_all && j_begin == 0 &&
+      j_count == n_all && n_all <= small_max_n((int)sizeof(R))) {
+    // small N, whole system: one evaluation of the small-N kernel (no partial slots)
+    V4<R>* p = const_cast<V4<R>*>(static_cast<const V4<R>*>(pos4));
+    cudaError_t e = launch_simulate_small<R>(a, kf, p, nullptr, -1, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) return NB_OK;
+    if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported)
+      return cuda_fail(e, "small_simulate_kernel");
+    cudaGetLastError();  // fall through to the stream-K pass
+  }
+  cudaError_t e = launch_step<R>(a, kf, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "launch_step");
   return NB_OK;
 }

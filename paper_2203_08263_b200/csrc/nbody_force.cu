@@ -957,10 +957,13 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
   // The epilogue thread of body il keeps its velocity and previous acceleration
   // in registers for the whole launch (it is the only one that updates them).
   const int64_t il = blockIdx.x * (int64_t)TB + tid;
+  // steps < 0: one force evaluation only (mode ACCEL: acc written, nothing moves)
   B vel{}, acc_prev{};
-  if (tid < TB && il < n) vel = a.vel[il];
-  for (int64_t st = 0; st <= steps; ++st) {
-    a.mode = st == 0 ? NB_STEP_MODE_FIRST : (st < steps ? NB_STEP_MODE_KICK_DRIFT : NB_STEP_MODE_FINAL);
+  if (tid < TB && il < n && steps >= 0) vel = a.vel[il];
+  const int64_t last = steps < 0 ? 0 : steps;
+  for (int64_t st = 0; st <= last; ++st) {
+    a.mode = steps < 0 ? NB_STEP_MODE_ACCEL
+                       : (st == 0 ? NB_STEP_MODE_FIRST : (st < steps ? NB_STEP_MODE_KICK_DRIFT : NB_STEP_MODE_FINAL));
     a.pos = (st & 1) ? pos_b : pos_a;
     a.pos_next = (st & 1) ? pos_a : pos_b;
     for (int64_t j = tid; j < n; j += SN_T) {  // positions moved last step: coherent loads
