@@ -134,7 +134,11 @@ int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i);
  * pos4_next    n_all entries (STEP_FIRST / STEP_KICK_DRIFT): rows
  *              [i_begin, i_begin+n_i) receive the drifted (x,y,z,m).  Must not
  *              alias pos4.
- * stream       a cudaStream_t (NULL = legacy default stream). */
+ * stream       a cudaStream_t (NULL = legacy default stream).
+ * Summation order: fixed per (n_i, j_count, GPU) -- results are bitwise
+ * reproducible run to run.  A whole-system NB_MODE_ACCEL call at small N (the
+ * small-N bounds of nb_dev_simulate_*) runs the small-N kernel, whose order
+ * differs from the per-step path's (parity-tolerance equal, not bitwise). */
 int nb_dev_step_f32(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i,
                     int64_t j_begin, int64_t j_count, double g, double eps2, double dt,
                     int mode, int flags, double* carry, int carry_mode, void* acc4,
