@@ -266,31 +266,95 @@ int host_flags(const R* m, int64_t n, double eps2) {
 }
 
 // RAII bag of device allocations for the host-pointer entry points.
-struct DevBufs {
+// Device buffers of the synchronous host entry points (nb_host_*), kept between
+// calls per device and only ever grown: a plugin-style caller (one
+// accel_soa per force evaluation) pays no cudaMalloc/cudaFree per call.  One
+// host call at a time (the mutex is held for the whole call).
+struct Arena {
   void* p[12] = {};
+  size_t cap[12] = {};
+  void* host = nullptr;  // pinned staging: each call's uploads (and then downloads) as one block
+  size_t host_cap = 0;
+};
+std::mutex g_arena_mu;
+Arena g_arenas[32];
+
+struct DevBufs {
+  std::lock_guard<std::mutex> lock{g_arena_mu};
+  Arena* A = nullptr;
   int n = 0;
   cudaError_t err = cudaSuccess;
-  void* alloc(size_t bytes) {
-    void* q = nullptr;
-    if (err == cudaSuccess) err = cudaMalloc(&q, bytes ? bytes : 16);
-    if (err == cudaSuccess) p[n++] = q;
-    return q;
+  DevBufs() {
+    int d = 0;
+    err = cudaGetDevice(&d);
+    A = &g_arenas[(unsigned)d % 32u];
   }
-  ~DevBufs() {
-    for (int k = 0; k < n; ++k) cudaFree(p[k]);
+  void* alloc(size_t bytes) {
+    if (err != cudaSuccess || n >= 12) {
+      if (err == cudaSuccess) err = cudaErrorMemoryAllocation;
+      return nullptr;
+    }
+    if (bytes == 0) bytes = 16;
+    const int k = n++;
+    if (A->cap[k] < bytes) {
+      if (A->p[k]) cudaFree(A->p[k]);
+      A->p[k] = nullptr;
+      A->cap[k] = 0;
+      err = cudaMalloc(&A->p[k], bytes);
+      if (err != cudaSuccess) return nullptr;
+      A->cap[k] = bytes;
+    }
+    return A->p[k];
+  }
+  void* pinned(size_t bytes) {
+    if (err != cudaSuccess) return nullptr;
+    if (A->host_cap < bytes) {
+      if (A->host) cudaFreeHost(A->host);
+      A->host = nullptr;
+      A->host_cap = 0;
+      err = cudaMallocHost(&A->host, bytes);
+      if (err != cudaSuccess) return nullptr;
+      A->host_cap = bytes;
+    }
+    return A->host;
   }
 };
 
+// One upload of `k` host columns (n elements each, or 3n for an (n,3) AoS block
+// when counts[c] == 3) through the pinned staging into consecutive device
+// columns at d0; and one download of consecutive device columns.  Stream 0,
+// synchronous where the host reads back.
 template <typename R>
-int h2d(void* dst, const R* src, int64_t n) {
-  NB_CUDA(cudaMemcpy(dst, src, sizeof(R) * n, cudaMemcpyHostToDevice));
+int upload_cols(DevBufs& B, R* d0, const R* const* cols, const int* counts, int k, int64_t n) {
+  size_t total = 0;
+  for (int c = 0; c < k; ++c) total += (size_t)counts[c] * n;
+  R* h = static_cast<R*>(B.pinned(total * sizeof(R)));
+  if (!h) return cuda_fail(B.err, "cudaMallocHost");
+  size_t off = 0;
+  for (int c = 0; c < k; ++c) {
+    std::memcpy(h + off, cols[c], (size_t)counts[c] * n * sizeof(R));
+    off += (size_t)counts[c] * n;
+  }
+  NB_CUDA(cudaMemcpyAsync(d0, h, total * sizeof(R), cudaMemcpyHostToDevice, 0));
   return NB_OK;
 }
 template <typename R>
-int d2h(R* dst, const void* src, int64_t n) {
-  NB_CUDA(cudaMemcpy(dst, src, sizeof(R) * n, cudaMemcpyDeviceToHost));
+int download_cols(DevBufs& B, const R* d0, R* const* cols, const int* counts, int k, int64_t n) {
+  size_t total = 0;
+  for (int c = 0; c < k; ++c) total += (size_t)counts[c] * n;
+  NB_CUDA(cudaStreamSynchronize(0));  // every upload from the staging has landed
+  R* h = static_cast<R*>(B.pinned(total * sizeof(R)));
+  if (!h) return cuda_fail(B.err, "cudaMallocHost");
+  NB_CUDA(cudaMemcpyAsync(h, d0, total * sizeof(R), cudaMemcpyDeviceToHost, 0));
+  NB_CUDA(cudaStreamSynchronize(0));
+  size_t off = 0;
+  for (int c = 0; c < k; ++c) {
+    std::memcpy(cols[c], h + off, (size_t)counts[c] * n * sizeof(R));
+    off += (size_t)counts[c] * n;
+  }
   return NB_OK;
 }
+
 
 template <typename R>
 int host_accel(const R* px, const R* py, const R* pz, const R* pos_aos, const R* m, int64_t n, double g,
@@ -298,30 +362,32 @@ int host_accel(const R* px, const R* py, const R* pz, const R* pos_aos, const R*
   if (n < 1) return fail(NB_ERR_ARG, "n must be >= 1");
   if (!m || !ax || !ay || !az || (!pos_aos && (!px || !py || !pz))) return fail(NB_ERR_ARG, "null host pointer");
   DevBufs B;
-  void* dm = B.alloc(sizeof(R) * n);
   void* dpos = B.alloc(sizeof(V4<R>) * n);
   void* dacc = B.alloc(sizeof(V4<R>) * n);
-  void* dx = B.alloc(sizeof(R) * 3 * n);
+  void* dx = B.alloc(sizeof(R) * 4 * n);
   const int64_t wsb = step_workspace_bytes<R>(n);
-  void* ws = B.alloc(wsb);
+  void* ws = B.alloc(wsb);  // scratch: no initialisation needed
   if (B.err != cudaSuccess) return cuda_fail(B.err, "cudaMalloc");
   R* d0 = static_cast<R*>(dx);
   int rc;
-  if ((rc = h2d<R>(dm, m, n))) return rc;
   if (pos_aos) {
-    if ((rc = h2d<R>(d0, pos_aos, 3 * n))) return rc;
-    NB_CUDA(launch_pack_aos<R>(d0, static_cast<R*>(dm), static_cast<V4<R>*>(dpos), n, 0));
+    const R* cols[2] = {pos_aos, m};
+    const int counts[2] = {3, 1};
+    if ((rc = upload_cols<R>(B, d0, cols, counts, 2, n))) return rc;
+    NB_CUDA(launch_pack_aos<R>(d0, d0 + 3 * n, static_cast<V4<R>*>(dpos), n, 0));
   } else {
-    if ((rc = h2d<R>(d0, px, n)) || (rc = h2d<R>(d0 + n, py, n)) || (rc = h2d<R>(d0 + 2 * n, pz, n))) return rc;
-    NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, static_cast<R*>(dm), static_cast<V4<R>*>(dpos), n, 0));
+    const R* cols[4] = {px, py, pz, m};
+    const int counts[4] = {1, 1, 1, 1};
+    if ((rc = upload_cols<R>(B, d0, cols, counts, 4, n))) return rc;
+    NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, d0 + 3 * n, static_cast<V4<R>*>(dpos), n, 0));
   }
-  NB_CUDA(cudaMemset(ws, 0, wsb));
   if ((rc = dev_step<R>(dpos, n, 0, n, 0, n, g, eps2, 0.0, NB_MODE_ACCEL, host_flags<R>(m, n, eps2),
                         nullptr, 0, dacc, nullptr, nullptr, ws, wsb, nullptr)))
     return rc;
   NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(dacc), d0, d0 + n, d0 + 2 * n, n, 0));
-  if ((rc = d2h<R>(ax, d0, n)) || (rc = d2h<R>(ay, d0 + n, n)) || (rc = d2h<R>(az, d0 + 2 * n, n))) return rc;
-  return NB_OK;
+  R* out[3] = {ax, ay, az};
+  const int counts[3] = {1, 1, 1};
+  return download_cols<R>(B, d0, out, counts, 3, n);
 }
 
 template <typename R>
@@ -329,54 +395,47 @@ int host_step(R* px, R* py, R* pz, R* vx, R* vy, R* vz, R* pos_aos, R* vel_aos, 
               const R* az, int64_t n, double dt) {
   if (n < 1) return fail(NB_ERR_ARG, "n must be >= 1");
   if (!ax || !ay || !az) return fail(NB_ERR_ARG, "null host pointer");
+  if (pos_aos ? !vel_aos : (!px || !py || !pz || !vx || !vy || !vz)) return fail(NB_ERR_ARG, "null host pointer");
   DevBufs B;
   void* dpos = B.alloc(sizeof(V4<R>) * n);
   void* dvel = B.alloc(sizeof(V4<R>) * n);
   void* dacc = B.alloc(sizeof(V4<R>) * n);
-  void* dx = B.alloc(sizeof(R) * 3 * n);
+  void* dx = B.alloc(sizeof(R) * 9 * n);
   if (B.err != cudaSuccess) return cuda_fail(B.err, "cudaMalloc");
   R* d0 = static_cast<R*>(dx);
   V4<R>* P = static_cast<V4<R>*>(dpos);
   V4<R>* V = static_cast<V4<R>*>(dvel);
   V4<R>* A = static_cast<V4<R>*>(dacc);
   int rc;
-  auto up_soa = [&](const R* x, const R* y, const R* z, V4<R>* out) -> int {
-    int r;
-    if ((r = h2d<R>(d0, x, n)) || (r = h2d<R>(d0 + n, y, n)) || (r = h2d<R>(d0 + 2 * n, z, n))) return r;
-    NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, nullptr, out, n, 0));
-    return NB_OK;
-  };
-  auto down_soa = [&](const V4<R>* in, R* x, R* y, R* z) -> int {
-    NB_CUDA(launch_unpack_soa<R>(in, d0, d0 + n, d0 + 2 * n, n, 0));
-    int r;
-    if ((r = d2h<R>(x, d0, n)) || (r = d2h<R>(y, d0 + n, n)) || (r = d2h<R>(z, d0 + 2 * n, n))) return r;
-    return NB_OK;
-  };
-  auto up_aos = [&](const R* xyz, V4<R>* out) -> int {
-    int r;
-    if ((r = h2d<R>(d0, xyz, 3 * n))) return r;
-    NB_CUDA(launch_pack_aos<R>(d0, nullptr, out, n, 0));
-    return NB_OK;
-  };
-  auto down_aos = [&](const V4<R>* in, R* xyz) -> int {
-    NB_CUDA(launch_unpack_aos<R>(in, d0, n, 0));
-    return d2h<R>(xyz, d0, 3 * n);
-  };
-  if ((rc = up_soa(ax, ay, az, A))) return rc;
+  // one upload: a (SoA) then positions and velocities (SoA columns or (n,3) blocks)
   if (pos_aos) {
-    if (!vel_aos) return fail(NB_ERR_ARG, "null host pointer");
-    if ((rc = up_aos(pos_aos, P)) || (rc = up_aos(vel_aos, V))) return rc;
+    const R* cols[5] = {ax, ay, az, pos_aos, vel_aos};
+    const int counts[5] = {1, 1, 1, 3, 3};
+    if ((rc = upload_cols<R>(B, d0, cols, counts, 5, n))) return rc;
+    NB_CUDA(launch_pack_aos<R>(d0 + 3 * n, nullptr, P, n, 0));
+    NB_CUDA(launch_pack_aos<R>(d0 + 6 * n, nullptr, V, n, 0));
   } else {
-    if (!px || !py || !pz || !vx || !vy || !vz) return fail(NB_ERR_ARG, "null host pointer");
-    if ((rc = up_soa(px, py, pz, P)) || (rc = up_soa(vx, vy, vz, V))) return rc;
+    const R* cols[9] = {ax, ay, az, px, py, pz, vx, vy, vz};
+    const int counts[9] = {1, 1, 1, 1, 1, 1, 1, 1, 1};
+    if ((rc = upload_cols<R>(B, d0, cols, counts, 9, n))) return rc;
+    NB_CUDA(launch_pack_soa<R>(d0 + 3 * n, d0 + 4 * n, d0 + 5 * n, nullptr, P, n, 0));
+    NB_CUDA(launch_pack_soa<R>(d0 + 6 * n, d0 + 7 * n, d0 + 8 * n, nullptr, V, n, 0));
   }
+  NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, nullptr, A, n, 0));
   NB_CUDA(launch_drift<R>(P, V, A, n, dt, 0));
+  // one download: positions then velocities
   if (pos_aos) {
-    if ((rc = down_aos(P, pos_aos)) || (rc = down_aos(V, vel_aos))) return rc;
-  } else {
-    if ((rc = down_soa(P, px, py, pz)) || (rc = down_soa(V, vx, vy, vz))) return rc;
+    NB_CUDA(launch_unpack_aos<R>(P, d0, n, 0));
+    NB_CUDA(launch_unpack_aos<R>(V, d0 + 3 * n, n, 0));
+    R* out[2] = {pos_aos, vel_aos};
+    const int counts[2] = {3, 3};
+    return download_cols<R>(B, d0, out, counts, 2, n);
   }
-  return NB_OK;
+  NB_CUDA(launch_unpack_soa<R>(P, d0, d0 + n, d0 + 2 * n, n, 0));
+  NB_CUDA(launch_unpack_soa<R>(V, d0 + 3 * n, d0 + 4 * n, d0 + 5 * n, n, 0));
+  R* out[6] = {px, py, pz, vx, vy, vz};
+  const int counts[6] = {1, 1, 1, 1, 1, 1};
+  return download_cols<R>(B, d0, out, counts, 6, n);
 }
 
 template <typename R>
@@ -389,28 +448,28 @@ int host_simulate(R* px, R* py, R* pz, R* vx, R* vy, R* vz, const R* m, int64_t 
   void* pb = B.alloc(sizeof(V4<R>) * n);
   void* dv = B.alloc(sizeof(V4<R>) * n);
   void* da = B.alloc(sizeof(V4<R>) * n);
-  void* dx = B.alloc(sizeof(R) * 4 * n);
+  void* dx = B.alloc(sizeof(R) * 7 * n);
   const int64_t wsb = step_workspace_bytes<R>(n);
-  void* ws = B.alloc(wsb);
+  void* ws = B.alloc(wsb);  // scratch: no initialisation needed
   if (B.err != cudaSuccess) return cuda_fail(B.err, "cudaMalloc");
   R* d0 = static_cast<R*>(dx);
   int rc;
-  if ((rc = h2d<R>(d0, px, n)) || (rc = h2d<R>(d0 + n, py, n)) || (rc = h2d<R>(d0 + 2 * n, pz, n)) ||
-      (rc = h2d<R>(d0 + 3 * n, m, n)))
-    return rc;
+  {
+    const R* cols[7] = {px, py, pz, m, vx, vy, vz};
+    const int counts[7] = {1, 1, 1, 1, 1, 1, 1};
+    if ((rc = upload_cols<R>(B, d0, cols, counts, 7, n))) return rc;
+  }
   NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, d0 + 3 * n, static_cast<V4<R>*>(pa), n, 0));
-  if ((rc = h2d<R>(d0, vx, n)) || (rc = h2d<R>(d0 + n, vy, n)) || (rc = h2d<R>(d0 + 2 * n, vz, n))) return rc;
-  NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, nullptr, static_cast<V4<R>*>(dv), n, 0));
-  NB_CUDA(cudaMemset(ws, 0, wsb));
+  NB_CUDA(launch_pack_soa<R>(d0 + 4 * n, d0 + 5 * n, d0 + 6 * n, nullptr, static_cast<V4<R>*>(dv), n, 0));
   int in_b = 0;
   if ((rc = dev_simulate<R>(pa, pb, dv, da, n, g, dt, eps2, steps, host_flags<R>(m, n, eps2), ws, wsb,
                             nullptr, &in_b)))
     return rc;
   NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(in_b ? pb : pa), d0, d0 + n, d0 + 2 * n, n, 0));
-  if ((rc = d2h<R>(px, d0, n)) || (rc = d2h<R>(py, d0 + n, n)) || (rc = d2h<R>(pz, d0 + 2 * n, n))) return rc;
-  NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(dv), d0, d0 + n, d0 + 2 * n, n, 0));
-  if ((rc = d2h<R>(vx, d0, n)) || (rc = d2h<R>(vy, d0 + n, n)) || (rc = d2h<R>(vz, d0 + 2 * n, n))) return rc;
-  return NB_OK;
+  NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(dv), d0 + 3 * n, d0 + 4 * n, d0 + 5 * n, n, 0));
+  R* out[6] = {px, py, pz, vx, vy, vz};
+  const int counts[6] = {1, 1, 1, 1, 1, 1};
+  return download_cols<R>(B, d0, out, counts, 6, n);
 }
 
 template <typename R>
