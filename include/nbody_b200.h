@@ -13,7 +13,9 @@
  *     implicitly.  `block` and `threads` are accepted and ignored: the GPU uses
  *     its own tiling and all SMs.  `recip` selects the algebraic form on the CPU;
  *     the GPU always evaluates m*d*rsqrt(d2)^3, which the reference pins as
- *     equivalent to both forms (pkg/tests/test_kernels.py:220-227).
+ *     equivalent to both forms (pkg/tests/test_kernels.py:220-227).  The library
+ *     keeps the device buffers and a pinned staging block of these calls between
+ *     calls (per device, grow-only); calls are serialized internally.
  *
  *  2. nb_dev_*   -- DEVICE pointers owned by the caller (e.g. torch tensors),
  *     stream-ordered, asynchronous.  These carry the packed HBM layout the
