@@ -240,6 +240,17 @@ int nb_update_f64(void* pos_next, const void* pos_cur, void* vel, const void* ac
  * unpacked into dev_cols (the mass column is left as is), D2H of the x, y, z
  * and vx, vy, vz columns into the same places of host_cols, and a synchronize
  * of `stream` before returning. */
+/* load_cols + simulate + store_cols in one call (an unsharded system, n_i = n):
+ * host_cols in (the column block above), host_cols out (x, y, z, vx, vy, vz of
+ * the final state; synchronizes `stream`); *final_in_b as for nb_dev_simulate_*. */
+int nb_dev_simulate_cols_f32(void* host_cols, void* dev_cols, void* pos4_a, void* pos4_b, void* vel4,
+                             void* acc4, int64_t n, double g, double dt, double eps2, int64_t steps,
+                             int flags, void* workspace, int64_t workspace_bytes, void* stream,
+                             int* final_in_b);
+int nb_dev_simulate_cols_f64(void* host_cols, void* dev_cols, void* pos4_a, void* pos4_b, void* vel4,
+                             void* acc4, int64_t n, double g, double dt, double eps2, int64_t steps,
+                             int flags, void* workspace, int64_t workspace_bytes, void* stream,
+                             int* final_in_b);
 int nb_dev_load_cols_f32(const void* host_cols, void* dev_cols, int64_t n, int64_t n_i,
                          void* pos4, void* vel4, void* stream);
 int nb_dev_load_cols_f64(const void* host_cols, void* dev_cols, int64_t n, int64_t n_i,

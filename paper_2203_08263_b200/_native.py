@@ -48,6 +48,7 @@ _ARGTYPES = {
     "nb_dev_unpack": [_p, _i64, _p, _p, _p, _p],
     "nb_force": [_p, _i64, _i64, _i64, _d, _d, _p, _p, _i64, _p],
     "nb_update": [_p, _p, _p, _p, _p, _i64, _d, _i, _p],
+    "nb_dev_simulate_cols": [_p, _p, _p, _p, _p, _p, _i64, _d, _d, _d, _i64, _i, _p, _i64, _p, ctypes.POINTER(_i)],
     "nb_dev_load_cols": [_p, _p, _i64, _i64, _p, _p, _p],
     "nb_dev_store_cols": [_p, _p, _i64, _i64, _p, _p, _p],
     "nb_dev_drift": [_p, _p, _p, _i64, _d, _p],

@@ -265,7 +265,6 @@ int host_flags(const R* m, int64_t n, double eps2) {
   return (mask ? NB_FLAG_EXCLUDE_SELF : 0) | (uniform ? NB_FLAG_UNIFORM_MASS : 0);
 }
 
-// RAII bag of device allocations for the host-pointer entry points.
 // Device buffers of the synchronous host entry points (nb_host_*), kept between
 // calls per device and only ever grown: a plugin-style caller (one
 // accel_soa per force evaluation) pays no cudaMalloc/cudaFree per call.  One
@@ -562,6 +561,19 @@ int dev_store_cols(const void* pos4, const void* vel4, int64_t n, int64_t n_i, v
 }
 
 template <typename R>
+int dev_simulate_cols(const void* host_cols, void* dev_cols, void* pos_a, void* pos_b, void* vel4, void* acc4,
+                      int64_t n, double g, double dt, double eps2, int64_t steps, int flags, void* ws,
+                      int64_t ws_bytes, void* stream, int* final_in_b) {
+  int rc = dev_load_cols<R>(host_cols, dev_cols, n, n, pos_a, vel4, stream);
+  if (rc) return rc;
+  int in_b = 0;
+  if ((rc = dev_simulate<R>(pos_a, pos_b, vel4, acc4, n, g, dt, eps2, steps, flags, ws, ws_bytes, stream, &in_b)))
+    return rc;
+  if (final_in_b) *final_in_b = in_b;
+  return dev_store_cols<R>(in_b ? pos_b : pos_a, vel4, n, n, dev_cols, const_cast<void*>(host_cols), stream);
+}
+
+template <typename R>
 int dev_drift(void* pos4, void* vel4, const void* acc4, int64_t n, double dt, void* stream) {
   if (n < 0) return fail(NB_ERR_ARG, "n must be >= 0");
   if (n == 0) return NB_OK;
@@ -748,6 +760,18 @@ int nb_update_f32(void* pos_next, const void* pos_cur, void* vel, const void* ac
 int nb_update_f64(void* pos_next, const void* pos_cur, void* vel, const void* acc, const void* acc_prev,
                   int64_t n_i, double dt, int mode, void* stream) {
   return dev_update<double>(pos_next, pos_cur, vel, acc, acc_prev, n_i, dt, mode, stream);
+}
+int nb_dev_simulate_cols_f32(void* host_cols, void* dev_cols, void* pos_a, void* pos_b, void* vel4, void* acc4,
+                             int64_t n, double g, double dt, double eps2, int64_t steps, int flags, void* ws,
+                             int64_t ws_bytes, void* stream, int* final_in_b) {
+  return dev_simulate_cols<float>(host_cols, dev_cols, pos_a, pos_b, vel4, acc4, n, g, dt, eps2, steps, flags, ws,
+                                  ws_bytes, stream, final_in_b);
+}
+int nb_dev_simulate_cols_f64(void* host_cols, void* dev_cols, void* pos_a, void* pos_b, void* vel4, void* acc4,
+                             int64_t n, double g, double dt, double eps2, int64_t steps, int flags, void* ws,
+                             int64_t ws_bytes, void* stream, int* final_in_b) {
+  return dev_simulate_cols<double>(host_cols, dev_cols, pos_a, pos_b, vel4, acc4, n, g, dt, eps2, steps, flags, ws,
+                                   ws_bytes, stream, final_in_b);
 }
 int nb_dev_load_cols_f32(const void* host_cols, void* dev_cols, int64_t n, int64_t n_i, void* pos4, void* vel4,
                          void* stream) {

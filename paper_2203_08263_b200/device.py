@@ -134,10 +134,9 @@ class DeviceState:
         self._h2d_done = None
         self._h2d_pending = False
 
-    def load(self, positions, velocities, masses: np.ndarray) -> None:
-        """(Re)initialise the resident state from host data -- (N,3) arrays or
-        (x, y, z) column tuples: contiguous column writes into the pinned staging,
-        one asynchronous H2D and two pack launches on the current stream."""
+    def _fill_staging(self, positions, velocities, masses) -> None:
+        """Write the column block (x, y, z, m of all N; vx, vy, vz of the owned
+        rows) into the pinned staging."""
         if self._h2d_pending:
             self._h2d_done.synchronize()  # staging still feeding the previous copy
         self.masses = np.ascontiguousarray(masses, dtype=self.dtype)
@@ -151,6 +150,37 @@ class DeviceState:
             h[k * n:(k + 1) * n] = positions[k]
             h[4 * n + k * max(ni, 1): 4 * n + k * max(ni, 1) + ni] = velocities[k][lo:hi]
         h[3 * n:4 * n] = self.masses
+
+    def _staged_columns(self):
+        n, ni = self.n, self.n_i
+        h = self._h_np
+        pos = tuple(np.array(h[k * n:(k + 1) * n]) for k in range(3))
+        vel = tuple(np.array(h[4 * n + k * max(ni, 1): 4 * n + k * max(ni, 1) + ni]) for k in range(3))
+        return pos, vel
+
+    def simulate_columns(self, positions, velocities, masses, g: float, dt: float, eps2: float, steps: int,
+                         flags: int):
+        """load + simulate + readback of an unsharded system in ONE native call
+        (nb_dev_simulate_cols): returns the final (x, y, z) and (vx, vy, vz)
+        columns as fresh host arrays."""
+        if self.i_begin != 0 or self.n_i != self.n:
+            raise ValueError("DeviceState.simulate_columns runs an unsharded system")
+        self._fill_staging(positions, velocities, masses)
+        hp, dp = self._cols_ptrs
+        final_in_b = ctypes.c_int(0)
+        _native.call("nb_dev_simulate_cols" + self.sfx, hp, dp, self.pos_a.data_ptr(), self.pos_b.data_ptr(),
+                     self.vel.data_ptr(), self.acc.data_ptr(), self.n, g, dt, eps2, steps, int(flags),
+                     self.ws.data_ptr(), self.ws_bytes, self.stream_ptr(), ctypes.byref(final_in_b))
+        self._h2d_pending = False  # the call synchronized the stream
+        self.cur_is_a = not final_in_b.value
+        return self._staged_columns()
+
+    def load(self, positions, velocities, masses: np.ndarray) -> None:
+        """(Re)initialise the resident state from host data -- (N,3) arrays or
+        (x, y, z) column tuples: contiguous column writes into the pinned staging,
+        one asynchronous H2D and two pack launches on the current stream."""
+        self._fill_staging(positions, velocities, masses)
+        n, ni = self.n, self.n_i
         # one native call: H2D of the column block + the two pack launches
         hp, dp = self._cols_ptrs
         _native.call("nb_dev_load_cols" + self.sfx, hp, dp, n, ni, self.pos_a.data_ptr(), self.vel.data_ptr(),
@@ -172,10 +202,7 @@ class DeviceState:
         hp, dp = self._cols_ptrs
         _native.call("nb_dev_store_cols" + self.sfx, self.pos_cur.data_ptr(), self.vel.data_ptr(), n, ni, dp, hp,
                      self.stream_ptr())
-        h = self._h_np
-        pos = tuple(np.array(h[k * n:(k + 1) * n]) for k in range(3))
-        vel = tuple(np.array(h[4 * n + k * max(ni, 1): 4 * n + k * max(ni, 1) + ni]) for k in range(3))
-        return pos, vel
+        return self._staged_columns()
 
     @classmethod
     def from_generator(cls, kind: str, n: int, seed: int, dtype,

@@ -270,9 +270,10 @@ _STATE_CACHE: dict = {}
 _STATE_LOCK = threading.RLock()
 
 
-def _resident_state(pos, vel, m, dtype):
+def _resident_state(pos, vel, m, dtype, load: bool = True):
     """A DeviceState for (N, precision, device), reused across calls so repeated
-    simulate() calls pay only the H2D/D2H of their own data, not allocation."""
+    simulate() calls pay only the H2D/D2H of their own data, not allocation
+    (``load=False``: the caller uploads itself)."""
     import torch
 
     from .device import DeviceState
@@ -282,7 +283,7 @@ def _resident_state(pos, vel, m, dtype):
         if len(_STATE_CACHE) >= 4:
             _STATE_CACHE.clear()
         st = _STATE_CACHE[key] = DeviceState(pos, vel, m, dtype)
-    else:
+    elif load:
         st.load(pos, vel, m)
     return st
 
@@ -310,10 +311,11 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
     from .device import kernel_flags
     m = np.asarray(sys_.masses, dtype)
     with _STATE_LOCK:
-        st = _resident_state(_columns(sys_, "positions"), _columns(sys_, "velocities"), m, dtype)
-        st.simulate(params.gravitational_constant, params.dt, params.softening_sq, params.steps,
-                    kernel_flags(m, params.softening_sq, dtype))
-        pos, vel = st.columns_host()
+        pc, vc = _columns(sys_, "positions"), _columns(sys_, "velocities")
+        st = _resident_state(pc, vc, m, dtype, load=False)
+        # upload, simulate and read back in one native call (nb_dev_simulate_cols)
+        pos, vel = st.simulate_columns(pc, vc, m, params.gravitational_constant, params.dt, params.softening_sq,
+                                       params.steps, kernel_flags(m, params.softening_sq, dtype))
     if _value(sys_.layout) != "soa":
         pos, vel = np.stack(pos, 1), np.stack(vel, 1)
     return type(sys_)(sys_.layout, sys_.precision, pos, vel, sys_.masses.copy())

@@ -23,3 +23,27 @@ for path in libs:
             f(*args)
         dt = (time.perf_counter() - t0) / reps
         print(f"{os.path.basename(path):28s} N={n:6d} {dt * 1e6:9.1f} us per nb_host_accel_soa_f64", flush=True)
+
+# the whole simulate through the host entry point vs the Python API (C1: N=1024, FP64, 10 steps)
+if os.environ.get("NB_HOST_SIM", "1") == "1":
+    sys.path.insert(0, REPO)
+    import paper_2203_08263_b200 as nb
+    cfg = nb.BASELINE_CONFIGS["C1"]
+    s, prm = cfg.system(), cfg.params()
+    L = ctypes.CDLL(libs[-1])
+    f = L.nb_host_simulate_soa_f64
+    f.argtypes = [p] * 7 + [i64, d, d, d, i64]
+    cols = [c.copy() for c in s.positions + s.velocities]
+    m = s.masses.copy()
+
+    def host_call():
+        for k in range(6):
+            cols[k][...] = (s.positions + s.velocities)[k]
+        assert f(*[c.ctypes.data for c in cols], m.ctypes.data, s.count, 1.0, prm.dt, prm.softening_sq, prm.steps) == 0
+    for name, fn in (("nb_host_simulate_soa_f64", host_call), ("paper_2203_08263_b200.simulate", lambda: nb.simulate(s, prm))):
+        fn(); fn()
+        t0 = time.perf_counter()
+        for _ in range(50):
+            fn()
+        print(f"C1 simulate via {name:32s} {(time.perf_counter() - t0) / 50 * 1e6:9.1f} us", flush=True)
+    print("checksums", nb.checksum(nb.simulate(s, prm)), np.sum((cols[0] + cols[1]) + cols[2]))
