@@ -28,6 +28,8 @@ VARIANTS = {
     "t128_k8_b2": {"NB_F32_T": 128, "NB_F32_K": 8, "NB_F32_MINB": 2, "NB_F32_EXP2_MASK": 37},
     "t128_k8_b2_q": {"NB_F32_T": 128, "NB_F32_K": 8, "NB_F32_MINB": 2, "NB_F32_EXP2_MASK": 33},
     "t128_k8_b1": {"NB_F32_T": 128, "NB_F32_K": 8, "NB_F32_MINB": 1, "NB_F32_EXP2_MASK": 37},
+    # FP64 geometry: more / fewer targets per thread
+    "f64_k8_t128": {"NB_F64_K": 8, "NB_F64_T": 128, "NB_F64_MINB": 2},
     "t512_k2": {"NB_F32_T": 512, "NB_F32_K": 2, "NB_F32_TJ": 512, "NB_F32_SUMS_IN_REGS": 1,
                 "NB_F32_EXP2_MASK": 1, "NB_F32_EXP2_PHASES": 4},
     "t512_k2_p3": {"NB_F32_T": 512, "NB_F32_K": 2, "NB_F32_TJ": 512, "NB_F32_SUMS_IN_REGS": 1,
