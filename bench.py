@@ -181,6 +181,24 @@ def _cpu_child(cfg_name: str, fixed_n: int, kind: str) -> None:
     print(json.dumps([rate, desc]))
 
 
+def host_cpu_topology() -> dict:
+    """Logical CPUs usable by this process and the physical cores behind them
+    (lscpu: distinct (socket, core) pairs), plus the CPU model."""
+    info = {"logical_cpus_in_affinity": len(os.sched_getaffinity(0)), "physical_cores": None, "model": None}
+    try:
+        out = subprocess.run(["lscpu", "-p=CPU,CORE,SOCKET"], capture_output=True, text=True, timeout=10).stdout
+        allowed = os.sched_getaffinity(0)
+        cores = {(ln.split(",")[2], ln.split(",")[1]) for ln in out.splitlines()
+                 if ln and not ln.startswith("#") and int(ln.split(",")[0]) in allowed}
+        info["physical_cores"] = len(cores) or None
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.startswith("Model name:"):
+                info["model"] = ln.split(":", 1)[1].strip()
+    except (OSError, ValueError, IndexError, subprocess.TimeoutExpired):
+        pass
+    return info
+
+
 # --------------------------------------------------------------------------- GPU arm
 
 def _dist_env():
@@ -188,6 +206,63 @@ def _dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+NCU = "/usr/local/cuda/bin/ncu"
+
+
+def measure_traffic(args, single_launch: bool) -> dict:
+    """roofline.traffic measured in this run: one ncu pass (DRAM read + write
+    bytes, --clock-control none) over one launch of the same kernel on the same
+    config, in a child process after the timed region (ncu serialises and
+    replays the kernel, so nothing it prints is a timing).  Falls back to the
+    committed ncu summary (profiles/ncu_summary.json) when ncu is unavailable."""
+    if args.no_traffic or not os.path.exists(NCU):
+        return {"traffic": load_traffic(args.config), "traffic_source": "profiles/ncu_summary.json (committed capture)"}
+    kname = "regex:small_simulate_kernel|simulate_kernel" if single_launch else "regex:step_kernel"
+    cmd = [NCU, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none",
+           "-k", kname, "--launch-skip", "1", "-c", "1", "--csv", "--print-units", "base",
+           sys.executable, os.path.abspath(__file__), "--traffic-child", args.config]
+    try:
+        import csv
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        total = 0.0
+        seen = 0
+        hdr = None
+        for row in csv.reader(ln for ln in r.stdout.splitlines() if ln.startswith('"')):
+            if hdr is None:
+                hdr = row
+                continue
+            rec = dict(zip(hdr, row))
+            if rec.get("Metric Name") in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(rec.get("Metric Unit"), 1)
+                total += float(rec["Metric Value"].replace(",", "")) * scale
+                seen += 1
+        if seen == 2:
+            return {"traffic": total, "traffic_unit": "bytes per launch (dram read + write)",
+                    "traffic_source": "ncu in this run: " + " ".join(cmd[1:12]) + " ... (one launch, cold L2)"}
+        why = f"ncu rc={r.returncode}: {(r.stderr or r.stdout)[-200:]}"
+    except (OSError, subprocess.TimeoutExpired, ValueError) as e:
+        why = f"ncu failed: {e}"
+    return {"traffic": load_traffic(args.config),
+            "traffic_source": "profiles/ncu_summary.json (committed capture; in-run ncu unavailable: %s)" % why}
+
+
+def _traffic_child(cfg_name: str) -> None:
+    """Two launches of the config's kernel for the in-run ncu pass (the first is
+    skipped): the same state, flags and code path as the timed simulate."""
+    import torch
+    import paper_2203_08263_b200 as nb
+    from paper_2203_08263_b200.device import DeviceState, kernel_flags
+    cfg = nb.BASELINE_CONFIGS[cfg_name]
+    s = cfg.system()
+    dtype = cfg.precision.dtype
+    st = DeviceState(s.position_matrix().astype(dtype), np.stack(s.velocities, 1), s.masses, dtype)
+    p = cfg.params()
+    flags = kernel_flags(s.masses, p.softening_sq, dtype)
+    for _ in range(2):
+        st.simulate(p.gravitational_constant, p.dt, p.softening_sq, p.steps, flags)
+    torch.cuda.synchronize()
 
 
 def load_traffic(config_name: str):
@@ -217,10 +292,13 @@ def run_ours(args) -> dict:
     # One process per GPU.  Test hook (never the measured configuration):
     # NB_BENCH_BACKEND=gloo with more ranks than GPUs runs the multi-rank driver
     # logic with ranks sharing a device and a host-side exchange.
+    backend = os.environ.get("NB_BENCH_BACKEND", "nccl")
+    if backend == "nccl" and world > torch.cuda.device_count():
+        raise SystemExit(f"--gpus {world} needs {world} visible GPUs (one process per GPU); "
+                         f"found {torch.cuda.device_count()}")
     local_dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_dev)
     dev = torch.device("cuda", local_dev)
-    backend = os.environ.get("NB_BENCH_BACKEND", "nccl")
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
@@ -339,7 +417,21 @@ def run_ours(args) -> dict:
     # per-launch kernel durations (N=1): the dominant (only) kernel of the step
     kernel_ms = [x for ms in launch_ms_all for x in ms]
     peak = nominal_peak_tflops(pbytes)
-    if kernel_ms:
+    launches_per_sim = launches / max(1, args.steps)
+    kernel_name = "nb::step_kernel (fused force + velocity-Verlet epilogue) + nb::fixup_kernel"
+    launch_timing = ("CUDA events between consecutive launches on the launch stream "
+                     "(nb_dev_simulate_timed), one simulate right after the timed steps")
+    single_launch = world == 1 and launches_per_sim == 1
+    if single_launch:
+        # Small N: the whole simulate is ONE cooperative launch (small_simulate_kernel
+        # or simulate_kernel), so the events around each timed step bracket exactly
+        # that kernel; its steps+1 force evaluations are the algorithmic work.
+        mean_launch_s = statistics.mean(step_ms) / 1e3
+        achieved = FLOP_PER_INTERACTION * float(cfg.n) * cfg.n * (steps + 1) / mean_launch_s / 1e12
+        kernel_name = ("nb::small_simulate_kernel" if cfg.n <= (4096 if pbytes == 4 else 2560)
+                       else "nb::simulate_kernel") + " (the whole simulate in one cooperative launch)"
+        launch_timing = "CUDA events around each timed step = around its single launch"
+    elif kernel_ms:
         mean_launch_s = statistics.mean(kernel_ms) / 1e3
         achieved = FLOP_PER_INTERACTION * float(cfg.n) * cfg.n / mean_launch_s / 1e12
     else:
@@ -352,13 +444,13 @@ def run_ours(args) -> dict:
                        % (128 if pbytes == 4 else 64),
         "peak_measured_microbench": MEASURED_FFMA_TFLOPS if pbytes == 4 else MEASURED_DFMA_TFLOPS,
         "frac_of_measured_microbench": achieved / (MEASURED_FFMA_TFLOPS if pbytes == 4 else MEASURED_DFMA_TFLOPS),
-        "kernel": "nb::step_kernel (fused force + velocity-Verlet epilogue) + nb::fixup_kernel",
+        "kernel": kernel_name,
         "mean_launch_ms": mean_launch_s * 1e3,
-        "launch_timing": "CUDA events between consecutive launches on the launch stream "
-                         "(nb_dev_simulate_timed), one simulate right after the timed steps",
-        "algorithmic_flop_per_launch": FLOP_PER_INTERACTION * float(cfg.n) * cfg.n,
-        "traffic": load_traffic(args.config),
+        "launch_timing": launch_timing,
+        "algorithmic_flop_per_launch": FLOP_PER_INTERACTION * float(cfg.n) * cfg.n * ((steps + 1) if single_launch else 1),
     }
+    roofline.update(measure_traffic(args, single_launch) if world == 1 else
+                    {"traffic": None, "traffic_source": "not measured for N > 1 (ncu profiles one GPU)"})
 
     # ---------------------------------------------------------------- e2e through the public API
     e2e = None
@@ -378,10 +470,20 @@ def run_ours(args) -> dict:
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
+        # Bytes each simulate() moves (whole job): N=1 uploads the column block
+        # x, y, z, m, vx, vy, vz (7 N) and reads back x, y, z, vx, vy, vz (6 N);
+        # a sharded rank uploads x, y, z, m of all padded bodies plus its own
+        # velocity rows and reads back all N positions and velocities.
+        if world == 1:
+            h2d, d2h = 7 * cfg.n * pbytes, 6 * cfg.n * pbytes
+        else:
+            h2d = world * (4 * npad + 3 * ni) * pbytes
+            d2h = world * 6 * cfg.n * pbytes
         e2e = {"value": interactions / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * npad * 4 * pbytes,
-               "d2h_bytes_per_step": 2 * cfg.n * 3 * pbytes,
-               "api": "paper_2203_08263_b200.simulate(ParticleSystem, SimParams) from host NumPy arrays",
+               "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "api": "paper_2203_08263_b200.simulate(ParticleSystem, SimParams) from host NumPy arrays"
+                      + (f" on each of {world} ranks (i-sharded; bytes summed over ranks)" if world > 1 else ""),
                "checksum": nb.checksum(final)}
 
     result = {
@@ -410,6 +512,7 @@ def run_ours(args) -> dict:
             what = "the reference's compiled accel_soa" if desc["kind"] == "reference" else "the oracle C port"
             result["cpu_baseline"] = {
                 "value": rate, "unit": UNIT, "cores": desc["cores"], "kind": desc["kind"],
+                "host_cpu": host_cpu_topology(),
                 "sample": f"mean of {desc['reps']} force evaluations (N^2 = {desc['n'] ** 2:.3e} "
                           f"interactions each, after one warm-up evaluation) of the {cfg.name} initial "
                           f"state through {what} (soa-recip, {desc['cores']} threads), "
@@ -419,11 +522,49 @@ def run_ours(args) -> dict:
     return result if rank == 0 else None
 
 
-def run_reference(args) -> dict:
-    """The reference's own CPU implementation of the path (oracle/_ref) on the
-    host cores; same config, metric and unit.  Rank 0 only."""
+BASELINE_REF = os.path.join(REPO, "baseline", "_ref")
+
+
+def _ref_child(cfg_name: str, n_s: int, reps: int, warm: int) -> None:
+    """The UNMODIFIED reference (baseline/_ref, pip-installed from /root/reference)
+    through its own public API: nbodybench.harness.measure on the config (its
+    first n_s bodies), variant soa-recip on every host thread -- the
+    reference's fastest rung -- so kernels.simulate runs its stock path
+    (compiled accel_soa + step_soa + NumPy _kick).  Prints one JSON list."""
+    sys.path.insert(0, BASELINE_REF)
+    import nbodybench as R
+    from nbodybench import harness
     import paper_2203_08263_b200 as nb
     from oracle import oracle as O
+    cfg = nb.BASELINE_CONFIGS[cfg_name]
+    assert "cext" in R.kernels.available_backends(), "reference compiled extension missing"
+    R.set_backend("cext")
+    threads = O.host_threads()
+    full = cfg.system()
+    prec = R.Precision(cfg.precision.value)
+
+    def init_fn(n, seed, precision, layout):  # the BASELINE generator, as a reference ParticleSystem
+        pos = tuple(np.ascontiguousarray(c[:n]) for c in full.positions)
+        vel = tuple(np.ascontiguousarray(c[:n]) for c in full.velocities)
+        return R.ParticleSystem(R.Layout.SOA, precision, pos, vel, np.ascontiguousarray(full.masses[:n]))
+
+    bc = harness.BenchConfig(n_bodies=n_s, steps=cfg.steps,
+                             variant=R.KernelVariant(R.Layout.SOA, R.MathForm.RECIPROCAL_MULTIPLY, None, threads),
+                             precision=prec, repetitions=reps, warmup_runs=warm,
+                             gravitational_constant=1.0, dt=cfg.dt, softening_sq=cfg.softening_sq)
+    res = harness.measure(bc, init_fn=init_fn)
+    print(json.dumps([res.times_s, res.checksum, res.gflops_mean, res.status, res.backend, threads,
+                      R.__file__]))
+
+
+def run_reference(args) -> dict:
+    """The reference's own CPU implementation of the path on the host cores;
+    same config, metric and unit.  Rank 0 only.  Primary: the installed
+    reference package's harness.measure -> kernels.simulate (stock code path)
+    on a bounded sample of the config's bodies; fallback (package missing or
+    unusable on this host): its compiled accel_soa (oracle/_ref), one force
+    evaluation per step."""
+    import paper_2203_08263_b200 as nb
     world, rank, _ = _dist_env()
     if rank != 0:
         return None
@@ -434,39 +575,91 @@ def run_reference(args) -> dict:
         return {"impl": "reference", "unavailable": "the reference's compiled CPU kernel and its C port "
                                                     "both failed on this host"}
     rate, desc = probe
-    if desc["kind"] != "reference":
-        from oracle import oracle as O
-        O.ref_available = lambda: False
-    # size the per-step sample so the whole run stays within ~3 minutes
+    # size the sample so the whole run (warm-up + timed simulates) stays within ~3 minutes
     budget = 150.0
-    per_step = desc["seconds"]
+    evals = cfg.steps + 1
+    per_sim_full = desc["seconds"] * evals
     n_s = cfg.n
-    if per_step * (args.steps + args.warmup) > budget:
-        n_s = int(cfg.n * (budget / (per_step * (args.steps + args.warmup))) ** 0.5) // 1024 * 1024
-        n_s = max(n_s, 4096)
+    if per_sim_full * (args.steps + args.warmup) > budget:
+        n_s = int(cfg.n * (budget / (per_sim_full * (args.steps + args.warmup))) ** 0.5) // 1024 * 1024
+        n_s = max(min(n_s, cfg.n), 1024)
+    base = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if cfg.precision.dtype.itemsize == 4 else "f64",
+            "data": "synthetic (BASELINE.json generator, seed 0)"}
+    cmd = [sys.executable, os.path.abspath(__file__), "--ref-child", args.config, str(n_s), str(args.steps),
+           str(args.warmup)]
+    got = None
+    if os.path.isdir(os.path.join(BASELINE_REF, "nbodybench")):
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
+            if r.returncode == 0 and r.stdout.strip():
+                got = json.loads(r.stdout.strip().splitlines()[-1])
+            else:
+                print(f"reference package run failed: rc={r.returncode} {r.stderr[-400:]}", file=sys.stderr)
+        except (subprocess.TimeoutExpired, ValueError) as e:
+            print(f"reference package run failed: {e}", file=sys.stderr)
+    if got is not None:
+        times, checksum, gflops_mean, status, backend, threads, where = got
+        total = float(sum(times))
+        value = float(n_s) * n_s * evals * len(times) / total
+        sample = (f"nbodybench.harness.measure (the installed reference, {os.path.relpath(where, REPO)}) on the "
+                  f"first {n_s} bodies of the {cfg.name} state, {cfg.steps} steps = {evals} force evaluations "
+                  f"per simulate, variant soa-recip on {threads} threads, backend {backend}; "
+                  f"{args.warmup} untimed warm-up + {len(times)} timed simulates (harness clock)")
+        return {**base, "value": value, "ms_per_step": total * 1e3 / len(times),
+                "config": {"workload": cfg.name, "n_bodies": cfg.n, "sample_bodies": n_s,
+                           "integrator_steps": cfg.steps, "force_evaluations_per_step": evals,
+                           "softening_sq": cfg.softening_sq, "dt": cfg.dt,
+                           "path": "nbodybench.kernels.simulate via harness.measure (stock)"},
+                "gflops_20": FLOP_PER_INTERACTION * value / 1e9,
+                "gflops_reference_convention": gflops_mean, "checksum": checksum, "status": status,
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                                 "host_cpu": host_cpu_topology(), "sample": sample},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+    # fallback: one force evaluation per step through the compiled accel_soa
+    from oracle import oracle as O
+    if desc["kind"] != "reference":
+        O.ref_available = lambda: False
+    n_f = max(min(cfg.n, int(n_s * evals ** 0.5) // 1024 * 1024), 1024)
     for _ in range(args.warmup):
-        cpu_reference_rate(cfg, sys0, fixed_n=n_s, reps=1, warm=False)
+        cpu_reference_rate(cfg, sys0, fixed_n=n_f, reps=1, warm=False)
     total, inter = 0.0, 0.0
     for _ in range(args.steps):
-        r, d = cpu_reference_rate(cfg, sys0, fixed_n=n_s, reps=1, warm=False)
+        r, d = cpu_reference_rate(cfg, sys0, fixed_n=n_f, reps=1, warm=False)
         total += d["seconds"]
-        inter += float(n_s) * n_s
+        inter += float(n_f) * n_f
     value = inter / total
-    sample = (f"per step one force evaluation of the first {n_s} bodies of the {cfg.name} state "
-              f"({float(n_s) ** 2:.3e} interactions) through the reference's compiled accel_soa "
-              f"(soa-recip, {desc['cores']} threads); simulate() is steps+1 such evaluations")
-    return {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32" if cfg.precision.dtype.itemsize == 4 else "f64",
-        "data": "synthetic (BASELINE.json generator, seed 0)",
-        "config": {"workload": cfg.name, "n_bodies": cfg.n, "sample_bodies": n_s},
-        "gflops_20": FLOP_PER_INTERACTION * value / 1e9,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": desc["cores"], "kind": desc["kind"],
-                         "sample": sample},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    sample = (f"per step one force evaluation of the first {n_f} bodies of the {cfg.name} state "
+              f"({float(n_f) ** 2:.3e} interactions) through the reference's compiled accel_soa "
+              f"(soa-recip, {desc['cores']} threads); simulate() is steps+1 such evaluations "
+              f"(installed reference package unavailable)")
+    return {**base, "value": value, "ms_per_step": total * 1e3 / args.steps,
+            "config": {"workload": cfg.name, "n_bodies": cfg.n, "sample_bodies": n_f,
+                       "path": "compiled accel_soa only (fallback)"},
+            "gflops_20": FLOP_PER_INTERACTION * value / 1e9,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": desc["cores"], "kind": desc["kind"],
+                             "host_cpu": host_cpu_topology(), "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def spawn_ranks(args, argv) -> int:
+    """``--gpus N > 1`` without a torchrun environment: re-run this script under
+    ``torch.distributed.run`` with one process per GPU (the driver's own launch
+    form), forwarding the ranks' output; rank 0 prints the one JSON line.
+    NCCL's communicator log stays on (NCCL_DEBUG=INFO, stderr) so the rank count
+    is visible in the log."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 def main(argv=None):
@@ -481,13 +674,25 @@ def main(argv=None):
                     help="N>1 position exchange: NCCL all-gather through torch.distributed (default), the same through the library's nb_comm_* C ABI, or the fused peer-store epilogue")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the in-run ncu DRAM-traffic pass")
+    ap.add_argument("--traffic-child", metavar="CONFIG", help=argparse.SUPPRESS)
+    ap.add_argument("--ref-child", nargs=4, metavar=("CONFIG", "N", "REPS", "WARM"), help=argparse.SUPPRESS)
     ap.add_argument("--cpu-child", nargs=3, metavar=("CONFIG", "N", "KIND"), help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
     if args.cpu_child:
         _cpu_child(args.cpu_child[0], int(args.cpu_child[1]), args.cpu_child[2])
         return
+    if args.traffic_child:
+        _traffic_child(args.traffic_child)
+        return
+    if args.ref_child:
+        c, n, reps, warm = args.ref_child
+        _ref_child(c, int(n), int(reps), int(warm))
+        return
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args, sys.argv[1:] if argv is None else list(argv)))
     res = run_reference(args) if args.impl == "reference" else run_ours(args)
     if res is not None:
         print(json.dumps(res), flush=True)

@@ -216,7 +216,9 @@ int nb_dev_unpack_f64(const void* in4, int64_t n, void* x, void* y, void* z, voi
  * nb_dev_simulate_*):
  * nb_force: acc_out[k] = G * sum_j m_j d / (|d|^2 + eps2)^(3/2) for the targets
  *   [i_begin, i_begin+n_i) of pos_all against all n_all sources (the self pair is
- *   excluded explicitly when (real)eps2 == 0); workspace as for nb_dev_step_*.
+ *   always excluded explicitly: the masses are device-resident, so an overflowing
+ *   self term m*eps2^-1.5 cannot be ruled out on the host); workspace as for
+ *   nb_dev_step_*.
  * nb_update: the step update of one shard's n_i rows with the reference's
  *   rounding (mode NB_STEP_FIRST / NB_STEP_KICK_DRIFT / NB_STEP_FINAL_KICK, as in
  *   the fused step): pos_next = drifted pos_cur (= pos_cur for the final kick),
@@ -324,6 +326,9 @@ int nb_comm_allgather_all(void* const* bufs, size_t bytes_per_rank, void* const*
                           void* const* streams, int ndev);
 int nb_comm_destroy(void* comm);
 
+/* "nbody_b200 <version> (sm_100a) src:<digest>": <digest> is the first 16 hex
+ * digits of the SHA-256 over the library's sources (paper_2203_08263_b200/csrc/*
+ * and this header) the build was compiled from. */
 const char* nb_version(void);
 /* Number of kernel launches this library has issued on the calling process. */
 int64_t nb_launch_count(void);

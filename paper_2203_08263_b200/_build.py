@@ -22,6 +22,26 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hid
 SOURCES = ["nbody_force.cu", "nbody_update.cu", "nbody_capi.cu"]
 
 
+def source_files() -> list:
+    """Every file the library is compiled from (sorted)."""
+    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h"))]
+    files.append(os.path.join(REPO, "include", "nbody_b200.h"))
+    return sorted(files)
+
+
+def source_digest() -> str:
+    """First 16 hex digits of SHA-256 over (relative path, content) of the
+    sources; compiled into nb_version() and checked by _native.verify_build."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in source_files():
+        h.update(os.path.relpath(f, REPO).encode() + b"\0")
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+        h.update(b"\0")
+    return h.hexdigest()[:16]
+
+
 def _stale(target: str, deps) -> bool:
     if not os.path.exists(target):
         return True
@@ -34,6 +54,17 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
     ["NB_CHECK"]) produce a variant build in its own ``objdir``."""
     OBJ_ = objdir
     os.makedirs(OBJ_, exist_ok=True)
+    digest = source_digest()
+    stamp = os.path.join(OBJ_, "digest.txt")
+    try:
+        with open(stamp) as f:
+            built_from = f.read().strip()
+    except OSError:
+        built_from = None
+    # the digest is compiled into every object: a source change anywhere rebuilds all
+    spec = digest + " " + " ".join(defines)
+    if built_from != spec:
+        force = True
     headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     headers.append(os.path.join(REPO, "include", "nbody_b200.h"))
     jobs = []
@@ -41,7 +72,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ_, src.replace(".cu", ".o"))
         if force or _stale(o, [s] + headers):
-            dflags = [f"-D{d}" for d in defines]
+            dflags = [f"-D{d}" for d in defines] + [f'-DNB_SRC_DIGEST="{digest}"']
             cmd = [NVCC, *ARCH, *FLAGS, *dflags, "-Xptxas", "-v", "-c", s, "-o", o] if verbose else \
                   [NVCC, *ARCH, *FLAGS, *dflags, "-c", s, "-o", o]
             jobs.append(cmd)
@@ -62,6 +93,8 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(link)}\n{r.stdout}\n{r.stderr}")
+    with open(stamp, "w") as f:
+        f.write(spec + "\n")
     return lib
 
 

@@ -98,6 +98,7 @@ def lib() -> ctypes.CDLL:
         L.nb_last_error.restype = ctypes.c_char_p
         L.nb_version.restype = ctypes.c_char_p
         L.nb_launch_count.restype = _i64
+        _check_digest(L)
         _lib = L
     return _lib
 
@@ -152,6 +153,23 @@ def launch_count() -> int:
 
 def version() -> str:
     return lib().nb_version().decode()
+
+
+def _check_digest(L) -> None:
+    from ._build import source_digest
+    want = source_digest()
+    got = L.nb_version().decode().rsplit("src:", 1)[-1]
+    if got != want:
+        raise ImportError(f"{LIB_PATH} was built from sources {got}, but the tree holds {want}: "
+                          "rebuild with `python -m paper_2203_08263_b200._build` (no stale prebuilt library "
+                          "stands in for the current sources)")
+
+
+def verify_build() -> str:
+    """Raise if the loaded library was not compiled from the sources in this
+    tree (nb_version()'s src: digest vs _build.source_digest()); returns the digest."""
+    _check_digest(lib())
+    return version().rsplit("src:", 1)[-1]
 
 
 def declared_symbols(header: str = HEADER) -> list:

@@ -261,7 +261,11 @@ int host_flags(const R* m, int64_t n, double eps2) {
     uniform = uniform && m[i] == m[0];
   }
   const double big = sizeof(R) == 4 ? 1e30 : 1e300;
-  const bool mask = !(e > 0.0) || !(mmax * (1.0 / e) / std::sqrt(e) < big);
+  // Uniform-mass kernels form eps2^-1.5 without m (m is applied once per body),
+  // so the test uses max(mmax, 1): a small uniform mass must not hide an
+  // overflowing self term.
+  const double mt = mmax > 1.0 ? mmax : 1.0;
+  const bool mask = !(e > 0.0) || !(mt * (1.0 / e) / std::sqrt(e) < big);
   return (mask ? NB_FLAG_EXCLUDE_SELF : 0) | (uniform ? NB_FLAG_UNIFORM_MASS : 0);
 }
 
@@ -496,10 +500,14 @@ int dev_unpack(const void* in4, int64_t n, void* x, void* y, void* z, void* stre
 
 // SURVEY.md 8(b)'s proposed minimal surface: the force pass alone and the update
 // alone (the product path fuses them; these serve hosts that schedule the two).
+// The masses are device-resident here, so whether the self term m*eps2^-1.5
+// would overflow cannot be decided on the host: the self pair is always masked
+// (one select per pair; a masked self pair and an unmasked finite one both add
+// exactly 0, so the result equals the fused path's whenever that is finite).
 template <typename R>
 int dev_force(const void* pos_all, int64_t n_all, int64_t i_begin, int64_t n_i, double eps2, double g,
               void* acc_out, void* workspace, int64_t workspace_bytes, void* stream) {
-  const int flags = eps2 > 0.0 && (R)eps2 > (R)0 ? 0 : NB_FLAG_EXCLUDE_SELF;
+  const int flags = NB_FLAG_EXCLUDE_SELF;
   return dev_step<R>(pos_all, n_all, i_begin, n_i, 0, n_all, g, eps2, 0.0, NB_MODE_ACCEL, flags, nullptr, 0,
                      acc_out, nullptr, nullptr, workspace, workspace_bytes, stream);
 }
@@ -974,7 +982,13 @@ int nb_comm_destroy(void* comm) {
   return NB_OK;
 }
 
-const char* nb_version(void) { return "nbody_b200 0.1.0 (sm_100a)"; }
+#ifndef NB_SRC_DIGEST
+#define NB_SRC_DIGEST "unknown"
+#endif
+// The digest of the sources this library was compiled from (_build.py passes it):
+// a prebuilt .so that travelled with a snapshot cannot pass for a rebuild of
+// different sources (_native.verify_build).
+const char* nb_version(void) { return "nbody_b200 0.2.0 (sm_100a) src:" NB_SRC_DIGEST; }
 int64_t nb_launch_count(void) { return g_launches.load(); }
 
 }  // extern "C"

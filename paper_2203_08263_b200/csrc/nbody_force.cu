@@ -234,6 +234,31 @@ __device__ __forceinline__ float w_reference_form(float d2, float m) {
 #endif
 }
 
+// ---------------------------------------------------------------- staged source tiles
+// Source body jj of a shared-memory tile of TJ bodies.  FP32 tiles hold packed
+// 16-byte (x,y,z,m) bodies.  FP64 tiles hold two planes of 16-byte halves,
+// (x,y)[TJ] then (z,m)[TJ]: the staging stores of a warp are then contiguous
+// 512-byte runs (4 wavefronts), where a packed 32-byte body per lane puts only
+// four lanes' halves in each 128-byte wavefront (8 wavefronts, 2x; the r01
+// ncu capture counted those as 5.6M shared-store bank conflicts per launch).
+// The inner loop's reads are warp-wide broadcasts either way.
+template <int TJ>
+__device__ __forceinline__ F4 tile_get(const F4* tb, int jj) { return tb[jj]; }
+template <int TJ>
+__device__ __forceinline__ D4 tile_get(const D4* tb, int jj) {
+  const double2* p = reinterpret_cast<const double2*>(tb);
+  const double2 a = p[jj], b = p[TJ + jj];
+  return D4{a.x, a.y, b.x, b.y};
+}
+template <int TJ>
+__device__ __forceinline__ void tile_put(F4* tb, int idx, const F4& v) { tb[idx] = v; }
+template <int TJ>
+__device__ __forceinline__ void tile_put(D4* tb, int idx, const D4& v) {
+  double2* p = reinterpret_cast<double2*>(tb);
+  p[idx] = make_double2(v.x, v.y);
+  p[TJ + idx] = make_double2(v.z, v.w);
+}
+
 // ---------------------------------------------------------------- FP32 core
 // K target bodies per thread as K/2 packed pairs.  The FP64 segment sums live in
 // shared memory (3*K doubles per thread, touched once per tile) so the inner
@@ -380,7 +405,7 @@ struct CoreF32 {
   template <int TJ>
   __device__ __forceinline__ void full_tile(const F4* tb) {
 #pragma unroll UNROLL_
-    for (int jj = 0; jj < TJ; ++jj) interact(tb[jj], jj);
+    for (int jj = 0; jj < TJ; ++jj) interact(tile_get<TJ>(tb, jj), jj);
   }
   __device__ __forceinline__ void end_tile() {
 #pragma unroll
@@ -430,7 +455,7 @@ struct CoreF64 {
   template <int TJ>
   __device__ __forceinline__ void full_tile(const D4* tb) {
 #pragma unroll UNROLL_
-    for (int jj = 0; jj < TJ; ++jj) interact(tb[jj], jj);
+    for (int jj = 0; jj < TJ; ++jj) interact(tile_get<TJ>(tb, jj), jj);
   }
   __device__ __forceinline__ void interact(const D4& pj, int jj) {
 #if NB_F64_STAGEWISE
@@ -639,7 +664,9 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
     }
     core.zero_sums();
 
-    constexpr bool kTma = TMA && !COH;
+    // (FP32 only: FP64 tiles are stored as planes, which a contiguous bulk copy
+    // does not produce.)
+    constexpr bool kTma = TMA && !COH && sizeof(R) == 4;
     // TMA staging: thread 0 arms the tile's mbarrier with its byte count and
     // issues the bulk copies; everyone waits on the barrier's current phase.
     auto issue_tile = [&](int buf, int64_t lo) {
@@ -671,7 +698,7 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
     auto store_tile = [&](int buf) {
 #pragma unroll
       for (int r = 0; r < PER; ++r) {
-        tile[buf][r * T + tid] = stage[r];
+        tile_put<TJ>(tile[buf], r * T + tid, stage[r]);
         if (Core::NEEDS_LM) tile_lm[buf][r * T + tid] = lg2_mufu((float)stage[r].w);
       }
     };
@@ -722,13 +749,13 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
         int jj = 0;
 #pragma unroll 1
         for (; jj + 4 <= count; jj += 4) {
-          core.interact(tb[jj], jj);
-          core.interact(tb[jj + 1], jj + 1);
-          core.interact(tb[jj + 2], jj + 2);
-          core.interact(tb[jj + 3], jj + 3);
+          core.interact(tile_get<TJ>(tb, jj), jj);
+          core.interact(tile_get<TJ>(tb, jj + 1), jj + 1);
+          core.interact(tile_get<TJ>(tb, jj + 2), jj + 2);
+          core.interact(tile_get<TJ>(tb, jj + 3), jj + 3);
         }
 #pragma unroll 1
-        for (; jj < count; ++jj) core.interact(tb[jj], jj);
+        for (; jj < count; ++jj) core.interact(tile_get<TJ>(tb, jj), jj);
       }
       core.end_tile();
       if (!kTma && more) store_tile(buf ^ 1);

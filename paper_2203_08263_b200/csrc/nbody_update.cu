@@ -99,7 +99,9 @@ constexpr int PK = 4;
 template <typename R>
 __global__ void __launch_bounds__(256) potential_kernel(const V4<R>* pos, int64_t n, double eps2, int64_t span,
                                                        double* phi) {
-  __shared__ double4 tile[256];
+  // Two planes of 16-byte halves (contiguous per-warp stores; see tile_put in
+  // nbody_force.cu): (x, y) and (z, m).
+  __shared__ double2 tile_xy[256], tile_zw[256];
   const int tid = threadIdx.x;
   const int64_t i0 = blockIdx.x * (256LL * PK) + tid;
   const int64_t jlo = blockIdx.y * span, jhi = min(n, jlo + span);
@@ -115,7 +117,8 @@ __global__ void __launch_bounds__(256) potential_kernel(const V4<R>* pos, int64_
     const int64_t j = j0 + tid;
     if (j < jhi) {
       const V4<R> q = pos[j];
-      tile[tid] = make_double4(q.x, q.y, q.z, q.w);
+      tile_xy[tid] = make_double2(q.x, q.y);
+      tile_zw[tid] = make_double2(q.z, q.w);
     }
     __syncthreads();
     const int cnt = (int)min((int64_t)256, jhi - j0);
@@ -127,7 +130,8 @@ __global__ void __launch_bounds__(256) potential_kernel(const V4<R>* pos, int64_
     }
 #pragma unroll 4
     for (int jj = 0; jj < cnt; ++jj) {
-      const double4 q = tile[jj];
+      const double2 qa = tile_xy[jj], qb = tile_zw[jj];
+      const double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
 #pragma unroll
       for (int k = 0; k < PK; ++k) {
         const double dx = q.x + nx[k], dy = q.y + ny[k], dz = q.z + nz[k];

@@ -39,7 +39,9 @@ def _self_mask(mmax: float, eps2: float, dtype: np.dtype) -> bool:
     if not e > 0.0:
         return True
     big = 1e30 if dtype == np.float32 else 1e300
-    return not (mmax * (1.0 / e) / math.sqrt(e) < big)
+    # max(mmax, 1): uniform-mass kernels form eps2^-1.5 without m, so a small
+    # uniform mass must not hide an overflowing self term (host_flags does the same).
+    return not (max(mmax, 1.0) * (1.0 / e) / math.sqrt(e) < big)
 
 
 def needs_self_mask(masses: np.ndarray, eps2: float, dtype) -> bool:

@@ -162,6 +162,26 @@ def _store(state, field: str, values: np.ndarray) -> None:
         data[...] = values
 
 
+_CTYPE = {np.dtype(np.float32): "float", np.dtype(np.float64): "double"}
+
+
+def _check_buffers(sys_) -> None:
+    """Every state array must already be in the system precision, as the
+    reference's typed buffers demand: its compiled backend raises the buffer
+    dtype ValueError at the FFI call (_accel_cy.pyx:114, fused type ``real``);
+    this raises the same before any device work instead of casting."""
+    want = _dtype(sys_)
+    if _value(sys_.layout) == "soa":
+        arrays = [*sys_.positions, *sys_.velocities, sys_.masses]
+    else:
+        arrays = [sys_.positions, sys_.velocities, sys_.masses]
+    for a in arrays:
+        got = np.asarray(a).dtype
+        if got != want:
+            raise ValueError(f"Buffer dtype mismatch, expected '{_CTYPE.get(want, want)}' but got "
+                             f"'{_CTYPE.get(got, got)}' (system precision is {_value(sys_.precision)})")
+
+
 def _check(sys_, variant, out) -> None:
     """Mirror of kernels/__init__.py:171-180."""
     if variant is not None:
@@ -197,6 +217,7 @@ def compute_accelerations(sys_, params, variant: Optional[KernelVariant] = None,
     if out is None:
         out = AccelerationBuffer.allocate(_count(sys_), _value(sys_.precision))
     _check(sys_, variant, out)
+    _check_buffers(sys_)
     pos = _matrix(sys_, "positions")
     m = np.asarray(sys_.masses, dtype)
     eps2 = params.softening_sq
@@ -218,6 +239,7 @@ def integrate_step(sys_, acc: AccelerationBuffer, params, variant: Optional[Kern
     from . import _native
     from .device import pack_bodies
     _check(sys_, variant, acc)
+    _check_buffers(sys_)
     dtype = _dtype(sys_)
     n = _count(sys_)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -293,6 +315,7 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
     system (same class, layout and precision); ``sys_`` is not modified."""
     if variant is not None:
         _check(sys_, variant, None)
+    _check_buffers(sys_)
     if params.steps < 1:
         raise ValueError("steps must be >= 1")
     n, dtype = _count(sys_), _dtype(sys_)

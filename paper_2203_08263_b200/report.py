@@ -10,7 +10,12 @@ best of R repetitions on a monotonic clock, checksum of the last final state
 
 The ``variant`` label is ``b200-<precision>-p<gpus>``; ``threads`` carries the
 GPU count (the reference's parallelism axis); GFLOPS use the reference
-convention 20*N^2*steps/t (harness.py:39-47).
+convention 20*N^2*steps/t (harness.py:39-47).  Defaults are the reference
+harness's own (BenchConfig, harness.py:55-71: double precision, seed 42,
+dt 0.01, eps2 1e-9, G 1, 5 repetitions, 1 warm-up; initial state from
+init_system, core.py:200-227), so a GPU row sits beside CPU rows of the same
+physics.  The 18-column schema has no dt/eps2 columns: when either differs from
+those defaults the variant label says so (``b200-f32-p1-dt0.001-eps2_0.001``).
 """
 
 from __future__ import annotations
@@ -24,7 +29,7 @@ from dataclasses import dataclass, field
 from datetime import datetime, timezone
 from typing import Callable, List, Optional, Sequence
 
-from .core import Precision, SimParams, checksum, format_checksum, uniform_cube
+from .core import Precision, SimParams, checksum, format_checksum, init_system
 from .kernels import simulate
 
 __all__ = ["CSV_HEADER", "GpuBenchConfig", "GpuBenchResult", "gflops", "measure", "result_row",
@@ -52,17 +57,22 @@ def gflops(n: int, steps: int, seconds: float) -> float:
     return FLOPS_PER_INTERACTION * float(n) * float(n) * float(steps) / (seconds * 1e9)
 
 
+#: harness.BenchConfig's defaults (harness.py:55-71).
+REFERENCE_DT = 0.01
+REFERENCE_EPS2 = 1e-9
+
+
 @dataclass(frozen=True)
 class GpuBenchConfig:
     n_bodies: int
     steps: int
-    precision: Precision = Precision.SINGLE
-    seed: int = 0
-    repetitions: int = 3
+    precision: Precision = Precision.DOUBLE
+    seed: int = 42
+    repetitions: int = 5
     warmup_runs: int = 1
     gravitational_constant: float = 1.0
-    dt: float = 1e-3
-    softening_sq: float = 1e-3
+    dt: float = REFERENCE_DT
+    softening_sq: float = REFERENCE_EPS2
     gpus: int = 1
 
     def sim_params(self) -> SimParams:
@@ -84,8 +94,16 @@ class GpuBenchResult:
 
     @property
     def variant_label(self) -> str:
-        p = "f32" if self.config.precision is Precision.SINGLE else "f64"
-        return f"b200-{p}-p{self.config.gpus}"
+        c = self.config
+        p = "f32" if c.precision is Precision.SINGLE else "f64"
+        label = f"b200-{p}-p{c.gpus}"
+        if c.dt != REFERENCE_DT:
+            label += f"-dt{c.dt:g}"
+        if c.softening_sq != REFERENCE_EPS2:
+            label += f"-eps2_{c.softening_sq:g}"
+        if c.gravitational_constant != 1.0:
+            label += f"-G{c.gravitational_constant:g}"
+        return label
 
 
 def _host_label() -> str:
@@ -97,7 +115,7 @@ def _host_label() -> str:
     return f"{platform.node() or 'unknown'}/{platform.machine()}/{os.cpu_count()}c/{dev}"
 
 
-def measure(config: GpuBenchConfig, *, init_fn: Callable = uniform_cube,
+def measure(config: GpuBenchConfig, *, init_fn: Callable = init_system,
             clock: Callable[[], float] = time.perf_counter,
             simulate_fn: Optional[Callable] = None) -> GpuBenchResult:
     """harness.measure's protocol (harness.py:120-162) around the GPU simulate."""

@@ -34,6 +34,14 @@ def test_version(lib):
     assert "sm_100a" in _native.version()
 
 
+def test_library_built_from_these_sources(lib):
+    """nb_version() carries the digest of the sources the library was compiled
+    from; loading a library built from other sources raises (no stale .so)."""
+    from paper_2203_08263_b200._build import source_digest
+    assert _native.version().endswith("src:" + source_digest())
+    assert _native.verify_build() == source_digest()
+
+
 def test_argument_errors_without_device(lib):
     with pytest.raises(_native.NativeError) as e:
         _native.call("nb_dev_step_f32", None, 0, 0, 0, 0, 0, 1.0, 0.0, 0.0, 0, 0, None, 0,

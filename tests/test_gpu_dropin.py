@@ -1,0 +1,135 @@
+"""Drop-in proof against the real reference, on the GPU box.
+
+``__graft_entry__.build()`` pip-installs the unmodified reference package into
+the git-ignored ``baseline/_ref`` (with its compiled ``_accel_cy``) and copies
+its test suite to ``baseline/_ref/_tests``; both travel with the snapshot, so
+nothing here reads /root/reference at run time.
+
+* the reference's harness (harness.measure, harness.py:120-162) drives this
+  package's ``simulate`` through its ``simulate_fn`` hook with the reference's
+  own ParticleSystem / SimParams / KernelVariant objects, and its checksum
+  matches the reference's CPU ``measure`` on the same configuration;
+* the reference's OWN test suite (test_kernels, test_harness, test_backends,
+  test_core, test_validation, test_cli, test_acceptance less the multi-minute
+  CPU performance gate) passes with this package registered as a backend of
+  the installed reference (``_BACKENDS["b200"]``, ``set_backend("b200")``,
+  kernels/__init__.py:38-79) and active by default -- both the ctypes backend
+  module and the Cython binding of INTEGRATION.md.
+"""
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(REPO, "baseline", "_ref")
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "nbodybench")),
+                                 reason="installed reference (baseline/_ref) missing: run __graft_entry__.build()")]
+
+
+@pytest.fixture(scope="module")
+def ref():
+    sys.path.insert(0, REF)
+    try:
+        import nbodybench
+        from nbodybench import harness
+        assert os.path.dirname(nbodybench.__file__).startswith(REF)
+        yield nbodybench, harness
+    finally:
+        sys.path.remove(REF)
+
+
+@pytest.mark.parametrize("prec,tol", [("double", 1e-9), ("single", 5e-4)])
+def test_reference_harness_measures_gpu_simulate(ref, prec, tol):
+    """harness.measure(BenchConfig(1024 bodies), simulate_fn=b200.simulate) with
+    the reference's own objects: the GPU checksum equals the reference CPU
+    measure's (cext backend, same config) within the reference's variant
+    tolerances (validation.py:33: 1e-9 double, 5e-4 single vs double), and the
+    returned systems are the reference's own class."""
+    import paper_2203_08263_b200 as b200
+    R, harness = ref
+    R.set_backend("cext")
+    variant = R.reference_variant()
+    seen = []
+
+    def sim(sys_, params, v):
+        out = b200.simulate(sys_, params, v)
+        seen.append(type(out))
+        return out
+
+    cfg = harness.BenchConfig(n_bodies=1024, steps=10, variant=variant, precision=R.Precision(prec),
+                              repetitions=2, warmup_runs=1)
+    gpu = harness.measure(cfg, simulate_fn=sim)
+    cpu64 = harness.measure(harness.BenchConfig(n_bodies=1024, steps=10, variant=variant, repetitions=1,
+                                                warmup_runs=0))
+    assert gpu.status == "ok" and cpu64.status == "ok"
+    assert all(t is R.ParticleSystem for t in seen)
+    rel = abs(gpu.checksum - cpu64.checksum) / abs(cpu64.checksum)
+    print(prec, "gpu", gpu.checksum, "cpu", cpu64.checksum, "rel", rel)
+    assert rel <= tol
+
+
+def test_reference_harness_golden_and_c1(ref):
+    """The reference's GOLDEN_SIM_CHECKSUM (N=256, 10 steps, seed 42, double;
+    pkg/tests/conftest.py:25-29, rtol 1e-12) and the BASELINE C1 known answer
+    (9.5618706445328652) through harness.measure with the GPU
+    simulate; the C1 state comes in through the harness's init_fn hook."""
+    import paper_2203_08263_b200 as b200
+    R, harness = ref
+    golden = harness.measure(harness.BenchConfig(n_bodies=256, steps=10, variant=R.reference_variant(),
+                                                 repetitions=1, warmup_runs=0), simulate_fn=b200.simulate)
+    assert abs(golden.checksum - 387.73663935192604) <= 1e-12 * 387.73663935192604
+    c1 = b200.BASELINE_CONFIGS["C1"]
+
+    def init_fn(n, seed, precision, layout):
+        s = c1.system()
+        return R.ParticleSystem(R.Layout.SOA, precision, tuple(s.positions), tuple(s.velocities), s.masses)
+
+    res = harness.measure(harness.BenchConfig(n_bodies=c1.n, steps=c1.steps, variant=R.reference_variant(),
+                                              repetitions=1, warmup_runs=0, dt=c1.dt, softening_sq=c1.softening_sq),
+                          init_fn=init_fn, simulate_fn=b200.simulate)
+    assert abs(res.checksum - 9.5618706445328652) <= 1e-12 * 9.5618706445328652
+
+
+def test_reference_object_precision_mismatch_raises(ref):
+    """A reference ParticleSystem whose buffers are not in its declared
+    precision raises ValueError before any device work (the reference's typed
+    buffers raise at the FFI call, _accel_cy.pyx:114)."""
+    import paper_2203_08263_b200 as b200
+    R, _ = ref
+    s = R.init_system(64, R.Seed(1))
+    bad = R.ParticleSystem(R.Layout.SOA, R.Precision.SINGLE, s.positions, s.velocities, s.masses)
+    with pytest.raises(ValueError, match="dtype mismatch"):
+        b200.simulate(bad, R.SimParams(1.0, 0.01, 1e-9, 1))
+
+
+@pytest.mark.parametrize("binding", ["python", "cython"])
+def test_reference_test_suite_with_b200_backend(binding, tmp_path):
+    """The reference's own tests with b200 registered in its _BACKENDS and active."""
+    tests = os.path.join(REF, "_tests")
+    if not os.path.isdir(tests):
+        pytest.skip("reference test suite copy (baseline/_ref/_tests) missing: run __graft_entry__.build()")
+    if binding == "cython" and not any(f.startswith("_accel_b200") and f.endswith(".so")
+                                       for f in os.listdir(os.path.join(REPO, "integration"))):
+        subprocess.run([sys.executable, os.path.join(REPO, "integration", "build.py")], check=True)
+    files = ["test_kernels.py", "test_harness.py", "test_backends.py", "test_core.py", "test_validation.py",
+             "test_cli.py", "test_acceptance.py"]
+    env = dict(os.environ, NB_REF_BINDING=binding, PYTHONPATH=os.pathsep.join([os.path.join(REPO, "tests"), REF]))
+    cmd = [sys.executable, "-m", "pytest", *[os.path.join(tests, f) for f in files], "-p", "ref_b200_plugin",
+           "-k", "not c5_directional_performance", "-v", "-p", "no:cacheprovider", "-o", "addopts=",
+           "--rootdir", str(tmp_path)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=str(tmp_path))
+    out = r.stdout
+    print(out[-3000:])
+    assert r.returncode == 0, out[-6000:] + r.stderr[-3000:]
+    assert "registered backend b200" in out and "active: b200" in out
+    b200_passed = [ln for ln in out.splitlines() if "[b200" in ln and "PASSED" in ln]
+    # every backend-parametrised reference test ran on b200 too
+    assert len(b200_passed) >= 25, len(b200_passed)
+    m = re.search(r"(\d+) passed", out)
+    assert m and int(m.group(1)) >= 100

@@ -103,6 +103,10 @@ def test_self_mask_rule():
     assert needs_self_mask(m, 1e-46, np.float32)       # rounds to 0 in FP32
     assert needs_self_mask(m, 1e-27, np.float32)       # m*eps2^-1.5 overflows FP32
     assert not needs_self_mask(m, 1e-4, np.float32)
+    # uniform-mass kernels form eps2^-1.5 without m: a small uniform mass must
+    # not hide an overflowing self term
+    assert needs_self_mask(np.full(4, 1e-10), 1e-26, np.float32)
+    assert needs_self_mask(np.full(4, 1e-10, np.float32), 1e-26, np.float32)
 
 
 def test_shard_arithmetic():
@@ -128,3 +132,20 @@ def test_empty_and_mismatched_inputs_rejected_before_device_work():
         nb.simulate_arrays(np.zeros((4, 3)), np.zeros((4, 3)), np.ones(4), -1.0, 1e-3, 1)
     with pytest.raises(ValueError):
         nb.system_from_arrays(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros(0))
+
+
+def test_precision_mismatch_rejected_before_device_work():
+    """A system whose arrays are not in its declared precision raises ValueError
+    before any device work, as the reference's typed buffers do at the FFI call
+    (_accel_cy.pyx:114); nothing is silently cast."""
+    pos = tuple(np.zeros(4) for _ in range(3))
+    vel = tuple(np.zeros(4) for _ in range(3))
+    bad = nb.ParticleSystem(nb.Layout.SOA, nb.Precision.SINGLE, pos, vel, np.ones(4))
+    with pytest.raises(ValueError, match="dtype mismatch"):
+        nb.simulate(bad, nb.SimParams(1.0, 1e-3, 1e-3, 1))
+    with pytest.raises(ValueError, match="dtype mismatch"):
+        nb.compute_accelerations(bad, nb.SimParams(1.0, 1e-3, 1e-3, 1))
+    mixed = nb.ParticleSystem(nb.Layout.AOS, nb.Precision.DOUBLE, np.zeros((4, 3)),
+                              np.zeros((4, 3), np.float32), np.ones(4))
+    with pytest.raises(ValueError, match="dtype mismatch"):
+        nb.simulate(mixed, nb.SimParams(1.0, 1e-3, 1e-3, 1))

@@ -8,10 +8,11 @@ import paper_2203_08263_b200 as nb
 from paper_2203_08263_b200 import report
 
 REF_SRC = "/root/reference/pkg/src"
+REPO_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _fake_result(gpus=1, prec=nb.Precision.SINGLE, n=131072):
-    cfg = report.GpuBenchConfig(n_bodies=n, steps=10, precision=prec, gpus=gpus)
+    cfg = report.GpuBenchConfig(n_bodies=n, steps=10, precision=prec, gpus=gpus, seed=0)
     r = report.GpuBenchResult(config=cfg, times_s=[0.08, 0.09], best_time_s=0.08, mean_time_s=0.085,
                               gflops_best=report.gflops(n, 10, 0.08), gflops_mean=report.gflops(n, 10, 0.085),
                               checksum=54.053778966743266, host_label="box/x86_64/16c/NVIDIA B200",
@@ -59,8 +60,58 @@ def test_reference_report_renders_gpu_rows(tmp_path):
     assert "b200-f32-p1" in md and "GFLOPS" in md
 
 
+def test_defaults_are_the_reference_harness_defaults():
+    """GpuBenchConfig defaults = harness.BenchConfig's (harness.py:55-71); a row of
+    other physics says so in its label, since the schema has no dt/eps2 column."""
+    c = report.GpuBenchConfig(n_bodies=256, steps=10)
+    assert (c.precision, c.seed, c.repetitions, c.warmup_runs, c.dt, c.softening_sq,
+            c.gravitational_constant) == (nb.Precision.DOUBLE, 42, 5, 1, 0.01, 1e-9, 1.0)
+    assert report.GpuBenchResult(config=c).variant_label == "b200-f64-p1"
+    odd = report.GpuBenchConfig(n_bodies=256, steps=10, precision=nb.Precision.SINGLE, dt=1e-3, softening_sq=1e-3)
+    assert report.GpuBenchResult(config=odd).variant_label == "b200-f32-p1-dt0.001-eps2_0.001"
+
+
 @pytest.mark.gpu
 def test_measure_on_gpu(tmp_path):
     r = report.measure(report.GpuBenchConfig(n_bodies=4096, steps=5, repetitions=2))
     assert r.status == "ok" and r.gflops_best > 0 and len(r.times_s) == 2
     report.emit_csv([r], str(tmp_path / "m.csv"))
+
+
+@pytest.mark.gpu
+def test_measure_golden_rows_through_reference_report(tmp_path):
+    """Real GPU rows through the CSV path: report.measure with the reference
+    harness defaults reproduces GOLDEN_SIM_CHECKSUM (N=256, 10 steps, seed 42;
+    pkg/tests/conftest.py:25-29) to 1e-12, the BASELINE C1 run reproduces the C1
+    known answer 9.5618706445328652 to 1e-12 -- in the CSV
+    text, i.e. after the 17-digit checksum formatting -- and the installed
+    reference's own read_rows/render_report (cli.py:435-545) accept the rows."""
+    import paper_2203_08263_b200 as nbb
+    golden = report.measure(report.GpuBenchConfig(n_bodies=256, steps=10, repetitions=2))
+    c1 = nbb.BASELINE_CONFIGS["C1"]
+    c1_cfg = report.GpuBenchConfig(n_bodies=c1.n, steps=c1.steps, seed=0, dt=c1.dt, softening_sq=c1.softening_sq,
+                                   repetitions=2)
+    c1_row = report.measure(c1_cfg, init_fn=lambda n, seed, prec: c1.system())
+    f32 = report.measure(report.GpuBenchConfig(n_bodies=256, steps=10, repetitions=2,
+                                               precision=nb.Precision.SINGLE))
+    path = tmp_path / "gpu.csv"
+    report.emit_csv([golden, c1_row, f32], str(path))
+    import csv as _csv
+    rows = list(_csv.DictReader(open(path)))
+    assert abs(float(rows[0]["checksum"]) - 387.73663935192604) <= 1e-12 * 387.73663935192604
+    assert abs(float(rows[1]["checksum"]) - 9.5618706445328652) <= 1e-12 * 9.5618706445328652
+    assert abs(float(rows[2]["checksum"]) - 387.73663935192604) <= 5e-4 * 387.73663935192604
+    assert [r["status"] for r in rows] == ["ok"] * 3
+    assert [r["variant"] for r in rows] == ["b200-f64-p1", "b200-f64-p1-eps2_0.01", "b200-f32-p1"]
+    ref = os.path.join(REPO_ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "nbodybench")):
+        pytest.skip("installed reference (baseline/_ref) missing: run __graft_entry__.build()")
+    sys.path.insert(0, ref)
+    try:
+        from nbodybench.cli import read_rows, render_report
+    finally:
+        sys.path.remove(ref)
+    parsed = read_rows(str(path))
+    assert [r["variant"] for r in parsed] == [r["variant"] for r in rows]
+    md = render_report(str(path))
+    assert "b200-f64-p1" in md
