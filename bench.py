@@ -61,7 +61,15 @@ def nominal_peak_tflops(precision_bytes: int) -> float:
 # --------------------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: NVML in-process every 5 ms plus one sample right at start and stop
+    (so even a sub-millisecond region, C1's, has samples); nvidia-smi as the
+    fallback when NVML is unavailable."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -69,9 +77,50 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, power_w, reason names)
+        self._stop = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _nvml_sample(self):
+        nv, h = self.nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except AttributeError:  # pragma: no cover
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        names = [n for n, attr in self.REASONS if bits & getattr(nv, attr, 0)]
+        self.samples.append((float(sm), float(mx), pw, names))
+
+    def _nvml_loop(self):
+        while not self._stop.wait(0.005):
+            try:
+                self._nvml_sample()
+            except Exception:  # pragma: no cover
+                break
 
     def start(self):
+        try:
+            self.nvml = self._nvml_handle()
+            self._nvml_sample()
+            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -86,7 +135,25 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def _summary(self, source: str) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": source}
+        sm = [x[0] for x in self.samples]
+        loaded = [x[0] for x in self.samples if x[2] > 300] or sm
+        reasons = sorted({n for x in self.samples for n in x[3]})
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(x[1] for x in self.samples),
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_max": max(x[2] for x in self.samples), "source": source}
+
     def stop(self) -> dict:
+        if self.nvml is not None:
+            self._stop.set()
+            self.thread.join(timeout=2)
+            try:
+                self._nvml_sample()
+            except Exception:  # pragma: no cover
+                pass
+            return self._summary("nvml (5 ms + start/stop samples)")
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -95,26 +162,17 @@ class ClockSampler:
         except subprocess.TimeoutExpired:  # pragma: no cover
             self.proc.kill()
         self.thread.join(timeout=2)
-        sm, smax, power, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
             try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-                power.append(float(parts[2]))
+                rec = (float(parts[0]), float(parts[1]), float(parts[2]))
             except ValueError:
                 continue
-            for name, flag in zip(names, parts[4:8]):
-                if flag.lower() == "active":
-                    reasons.add(name)
-        loaded = [s for s, p in zip(sm, power) if p > 300] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm),
-                "power_w_max": max(power) if power else None}
+            self.samples.append((*rec, [n for n, flag in zip(names, parts[4:8]) if flag.lower() == "active"]))
+        return self._summary("nvidia-smi -lms 100")
 
 
 # --------------------------------------------------------------------------- CPU baseline

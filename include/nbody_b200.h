@@ -243,8 +243,11 @@ int nb_update_f64(void* pos_next, const void* pos_cur, void* vel, const void* ac
  * and vx, vy, vz columns into the same places of host_cols, and a synchronize
  * of `stream` before returning. */
 /* load_cols + simulate + store_cols in one call (an unsharded system, n_i = n):
- * host_cols in (the column block above), host_cols out (x, y, z, vx, vy, vz of
- * the final state; synchronizes `stream`); *final_in_b as for nb_dev_simulate_*. */
+ * host_cols in (the column block above, 7n elements), host_cols out (x, y, z,
+ * vx, vy, vz of the final state, masses unchanged; one H2D and one D2H of the
+ * block; synchronizes `stream`); *final_in_b as for nb_dev_simulate_*.  At
+ * small N the simulate kernel reads and writes dev_cols itself (no pack/unpack
+ * launches); pos4_a/b, vel4 and acc4 hold the final state either way. */
 int nb_dev_simulate_cols_f32(void* host_cols, void* dev_cols, void* pos4_a, void* pos4_b, void* vel4,
                              void* acc4, int64_t n, double g, double dt, double eps2, int64_t steps,
                              int flags, void* workspace, int64_t workspace_bytes, void* stream,

@@ -118,7 +118,6 @@ int make_step_args(StepArgs<R>& a, const void* pos4, int64_t n_all, int64_t i_be
   if (!workspace || workspace_bytes < need)
     return fail(NB_ERR_WORKSPACE, "workspace smaller than nb_dev_workspace_bytes(): need " + std::to_string(need));
 
-  const StepGeometry geo = step_geometry<R>(n_i, j_count);
   a = StepArgs<R>{};
   a.pos = static_cast<const V4<R>*>(pos4);
   a.n_all = n_all; a.i_begin = i_begin; a.n_i = n_i; a.j_begin = j_begin; a.j_count = j_count;
@@ -129,7 +128,8 @@ int make_step_args(StepArgs<R>& a, const void* pos4, int64_t n_all, int64_t i_be
   a.acc = static_cast<V4<R>*>(acc4);
   a.vel = static_cast<V4<R>*>(vel4);
   a.pos_next = static_cast<V4<R>*>(pos4_next);
-  a.slots = reinterpret_cast<double*>(static_cast<char*>(workspace) + counters_bytes(geo.n_iblocks));
+  a.flags = static_cast<unsigned long long*>(workspace);
+  a.slots = reinterpret_cast<double*>(static_cast<char*>(workspace) + workspace_header_bytes<R>());
   a.n_peers = n_peers;
   for (int q = 0; q < n_peers; ++q) a.peers[q] = static_cast<V4<R>*>(peers[q]);
   (void)stream;
@@ -165,13 +165,18 @@ int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int6
 
 // `events` (optional): steps+2 recorded events, one before every launch and one
 // after the last, so a caller can time each force evaluation on the stream.
+// cols (optional): the host API's device column block (x, y, z, m, vx, vy, vz;
+// n each).  The small-N kernel then reads the initial state from it and writes
+// the final state back (*cols_done = 1); every other path packs it into pos_a /
+// vel4 here first and leaves the unpack to the caller (*cols_done = 0).
 template <typename R>
 int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, double g, double dt,
                  double eps2, int64_t steps, int flags, void* ws, int64_t ws_bytes, void* stream,
-                 int* final_in_b, cudaEvent_t* events = nullptr) {
+                 int* final_in_b, cudaEvent_t* events = nullptr, R* cols = nullptr, int* cols_done = nullptr) {
   if (steps < 1) return fail(NB_ERR_ARG, "steps must be >= 1");
   if (!(dt > 0.0)) return fail(NB_ERR_ARG, "dt must be positive");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cols_done) *cols_done = 0;
   if (!events && n <= small_max_n((int)sizeof(R))) {
     // small N: whole loop in one cooperative launch, source split inside the CTA
     StepArgs<R> a;
@@ -180,15 +185,21 @@ int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, do
     if (rc && rc != -1) return rc;
     if (rc == 0) {
       cudaError_t e = launch_simulate_small<R>(a, flags & (NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS),
-                                               static_cast<V4<R>*>(pos_a), static_cast<V4<R>*>(pos_b), steps, st);
+                                               static_cast<V4<R>*>(pos_a), static_cast<V4<R>*>(pos_b), steps, st,
+                                               cols);
       if (e == cudaSuccess) {
         if (final_in_b) *final_in_b = (steps & 1) ? 1 : 0;
+        if (cols_done) *cols_done = cols ? 1 : 0;
         return NB_OK;
       }
       if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported)
         return cuda_fail(e, "small_simulate_kernel");
       cudaGetLastError();  // fall through to the stream-K paths
     }
+  }
+  if (cols) {  // the stream-K paths read the packed rows
+    NB_CUDA(launch_pack_soa<R>(cols, cols + n, cols + 2 * n, cols + 3 * n, static_cast<V4<R>*>(pos_a), n, st));
+    NB_CUDA(launch_pack_soa<R>(cols + 4 * n, cols + 5 * n, cols + 6 * n, nullptr, static_cast<V4<R>*>(vel4), n, st));
   }
   if (!events && n <= persistent_max_n()) {
     // small N: the whole loop in one cooperative launch (launch-bound otherwise)
@@ -572,13 +583,30 @@ template <typename R>
 int dev_simulate_cols(const void* host_cols, void* dev_cols, void* pos_a, void* pos_b, void* vel4, void* acc4,
                       int64_t n, double g, double dt, double eps2, int64_t steps, int flags, void* ws,
                       int64_t ws_bytes, void* stream, int* final_in_b) {
-  int rc = dev_load_cols<R>(host_cols, dev_cols, n, n, pos_a, vel4, stream);
+  // One H2D of the column block; the simulate reads it directly (small N) or
+  // packs it itself; then the unpack (if the simulate did not write the columns)
+  // and one D2H of positions and velocities.
+  if (n < 1) return fail(NB_ERR_ARG, "need n >= 1");
+  if (!host_cols || !dev_cols || !pos_a || !pos_b || !vel4 || !acc4) return fail(NB_ERR_ARG, "null pointer");
+  if (!aligned16(pos_a) || !aligned16(vel4)) return fail(NB_ERR_ARG, "pos4/vel4 must be 16-byte aligned");
+  if (cudaError_t be = bind_device_of(pos_a)) return cuda_fail(be, "pos4 is not a device pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  R* d = static_cast<R*>(dev_cols);
+  NB_CUDA(cudaMemcpyAsync(d, host_cols, (size_t)(7 * n) * sizeof(R), cudaMemcpyHostToDevice, st));
+  int in_b = 0, done = 0;
+  int rc = dev_simulate<R>(pos_a, pos_b, vel4, acc4, n, g, dt, eps2, steps, flags, ws, ws_bytes, stream, &in_b,
+                           nullptr, d, &done);
   if (rc) return rc;
-  int in_b = 0;
-  if ((rc = dev_simulate<R>(pos_a, pos_b, vel4, acc4, n, g, dt, eps2, steps, flags, ws, ws_bytes, stream, &in_b)))
-    return rc;
   if (final_in_b) *final_in_b = in_b;
-  return dev_store_cols<R>(in_b ? pos_b : pos_a, vel4, n, n, dev_cols, const_cast<void*>(host_cols), stream);
+  if (!done) {
+    NB_CUDA(launch_unpack_soa<R>(static_cast<const V4<R>*>(in_b ? pos_b : pos_a), d, d + n, d + 2 * n, n, st));
+    NB_CUDA(launch_unpack_soa<R>(static_cast<const V4<R>*>(vel4), d + 4 * n, d + 5 * n, d + 6 * n, n, st));
+  }
+  // one D2H of the whole block (the masses ride along unchanged: one copy's
+  // latency instead of two at small N)
+  NB_CUDA(cudaMemcpyAsync(const_cast<void*>(host_cols), d, (size_t)(7 * n) * sizeof(R), cudaMemcpyDeviceToHost, st));
+  NB_CUDA(cudaStreamSynchronize(st));
+  return NB_OK;
 }
 
 template <typename R>

@@ -36,9 +36,11 @@
 #include "nbody_common.cuh"
 #include "nbody_kernels.h"
 
+#include <atomic>
 #include <cooperative_groups.h>
 #include <cstdlib>
 #include <mutex>
+#include <random>
 
 // Tuning knobs (overridable with -D for variant sweeps, tools/variants.py).
 #ifndef NB_F32_K
@@ -620,9 +622,58 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// ---------------------------------------------------------------- split i-block fixup
+// Ready flags of the partial slots (in-kernel fixup): a slot's flag holds the
+// launch's unique tag once its partials are visible at GPU scope.
+__device__ __forceinline__ void flag_publish(unsigned long long* f, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long flag_load(const unsigned long long* f) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+  return v;
+}
+
+// The partial slot CTA cc of split i-block b wrote its segment of b into: a
+// CTA's first segment goes to slot 2c, its last (when it has two) to 2c+1; so
+// the first contributor cf used 2cf+1 unless its units start exactly at b.
+__device__ __forceinline__ int64_t slot_of(const Sched& S, int64_t NT, int64_t b, int64_t cf, int64_t cc) {
+  return (cc == cf && S.start(cf) != b * NT) ? 2 * cf + 1 : 2 * cc;
+}
+
+// One target body of a split i-block: the FP64 partials of the contributing
+// CTAs cf..cl summed in ascending CTA order (L2 loads: other CTAs of this or an
+// earlier launch wrote them), then the epilogue.
+template <typename R, int IB>
+__device__ __forceinline__ void fixup_one(const StepArgs<R>& a, const Sched& S, int64_t b, int64_t o, int64_t cf,
+                                          int64_t cl) {
+  const int64_t il = b * IB + o;
+  double tx = 0.0, ty = 0.0, tz = 0.0;
+  for (int64_t cc = cf; cc <= cl; ++cc) {
+    const int64_t sl = slot_of(S, a.n_tiles, b, cf, cc);
+    NB_DCHECK(sl >= 0 && sl < 2 * a.grid && cc < a.grid && o < IB);
+    const double* q = a.slots + sl * 3 * IB + o;
+    tx += __ldcg(q);
+    ty += __ldcg(q + IB);
+    tz += __ldcg(q + 2 * IB);
+  }
+  finalize_body<R>(a, il, tx, ty, tz);
+}
+
 // One force(+update) pass of the stream-K decomposition: the body of
 // step_kernel, shared with the persistent multi-step simulate_kernel.
-template <class Core, int T, int TJ, int CH, bool COH, bool TMA>
+//
+// INFIX: split i-blocks are finished inside this launch instead of by
+// fixup_kernel.  Every contributor publishes its slot with a ready flag; after
+// its last unit a CTA waits for the flags of the (at most two) split i-blocks it
+// contributed to and finishes its own 1/m share of their bodies (m
+// contributors), summing the slots in the same ascending CTA order as
+// fixup_kernel -- bitwise the same result, one kernel boundary per step fewer,
+// and the fixup spread over all contributors.  Waiting on other CTAs of the
+// launch is safe because the persistent grid is at most one wave (every CTA is
+// resident; launch_step falls back to fixup_kernel otherwise) and a CTA only
+// ever waits on CTAs of its own launch.
+template <class Core, int T, int TJ, int CH, bool COH, bool TMA, bool INFIX = false>
 __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
                                           V4<typename Core::R> (*tile)[TJ], double* s_sums,
                                           uint64_t* mbar) {
@@ -786,6 +837,13 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
         sp[IB + k * T + tid] = core.sum(1, k);
         sp[2 * IB + k * T + tid] = core.sum(2, k);
       }
+      if (INFIX) {  // every thread's partials, then the slot's ready flag (release at GPU scope)
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          flag_publish(a.flags + slot, a.tag);
+        }
+      }
     }
 #if NB_TRACE
     __syncthreads();
@@ -795,10 +853,31 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
 #endif
     u += t1 - t0;
   }
+  if constexpr (INFIX) {
+    // The split i-blocks this CTA contributed to hold its first and its last unit.
+    const int64_t bf = u_begin / NT, bl = (u_end - 1) / NT;
+    for (int pass = 0; pass < 2 && u_end > u_begin; ++pass) {
+      const int64_t b = pass == 0 ? bf : bl;
+      if (pass == 1 && bl == bf) break;
+      const int64_t cf = S.cta_of(b * NT), cl = S.cta_of(b * NT + NT - 1);
+      if (cf == cl) continue;  // finished whole by its one CTA
+      if (tid < 32) {  // warp 0: one lane per contributor polls its slot's flag
+        for (int64_t cc = cf + tid; cc <= cl; cc += 32) {
+          const unsigned long long* f = a.flags + slot_of(S, NT, b, cf, cc);
+          while (flag_load(f) != a.tag) __nanosleep(64);
+        }
+      }
+      __syncthreads();
+      const int64_t m = cl - cf + 1, r = c - cf;
+      const int64_t rows = min((int64_t)IB, a.n_i - b * IB);
+      const int64_t o1 = (r + 1) * rows / m;
+      for (int64_t o = r * rows / m + tid; o < o1; o += T) fixup_one<R, IB>(a, S, b, o, cf, cl);
+    }
+  }
   if (a.n_peers) __threadfence_system();  // peer stores visible before the rank barrier
 }
 
-template <class Core, int T, int TJ, int MINB, int CH, bool TMA>
+template <class Core, int T, int TJ, int MINB, int CH, bool TMA, bool INFIX>
 __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename Core::R> a) {
   __shared__ alignas(128) V4<typename Core::R> tile[2][TJ];
   __shared__ double s_sums[Core::SMEM_SUMS * T];
@@ -817,7 +896,7 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
   asm volatile("griddepcontrol.wait;" ::: "memory");
   NB_TRACE_WAITED();
   asm volatile("griddepcontrol.launch_dependents;");
-  step_body<Core, T, TJ, CH, false, TMA>(a, tile, s_sums, mbar);
+  step_body<Core, T, TJ, CH, false, TMA, INFIX>(a, tile, s_sums, mbar);
   NB_TRACE_END(1);
 }
 
@@ -849,16 +928,7 @@ __device__ __forceinline__ void fixup_body(const StepArgs<R>& a, int64_t il) {
   const int64_t b = il / IB, o = il - b * IB;
   const int64_t cf = S.cta_of(b * NT), cl = S.cta_of(b * NT + NT - 1);
   if (cf == cl) return;
-  int64_t sl = (S.start(cf) == b * NT) ? 2 * cf : 2 * cf + 1;
-  double tx = 0.0, ty = 0.0, tz = 0.0;
-  for (int64_t cc = cf; cc <= cl; ++cc, sl = 2 * cc) {
-    NB_DCHECK(sl >= 0 && sl < 2 * a.grid && cc < a.grid && o < IB);
-    const double* q = a.slots + sl * 3 * IB + o;
-    tx += q[0];
-    ty += q[IB];
-    tz += q[2 * IB];
-  }
-  finalize_body<R>(a, il, tx, ty, tz);
+  fixup_one<R, IB>(a, S, b, o, cf, cl);
 }
 
 // ---------------------------------------------------------------- persistent multi-step kernel
@@ -942,11 +1012,15 @@ __host__ __device__ inline int64_t small_split_stride(int64_t n, int splits) {
 template <bool M, bool U> struct SmallF32 : CoreF32<2, M, 4, U> { static constexpr bool MASK_SELF = M; };
 template <bool M, bool U> struct SmallF64 : CoreF64<2, M, 4, U> { static constexpr bool MASK_SELF = M; };
 
+// cols (optional): simulate()'s device column block (x, y, z, m at 0, n, 2n, 3n;
+// vx, vy, vz at 4n, 5n, 6n).  Step 0 then reads the initial state straight from
+// the columns and the last step writes the final positions and velocities back
+// into them, so the host API needs no pack/unpack launches around the simulate.
 template <class Core, int PPW>
 __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename Core::R> a,
                                                               V4<typename Core::R>* pos_a,
                                                               V4<typename Core::R>* pos_b, int64_t steps,
-                                                              int64_t L) {
+                                                              int64_t L, typename Core::R* cols) {
   using R = typename Core::R;
   using B = V4<R>;
   constexpr int G = 32 / PPW;        // lane groups per warp
@@ -986,7 +1060,15 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
   const int64_t il = blockIdx.x * (int64_t)TB + tid;
   // steps < 0: one force evaluation only (mode ACCEL: acc written, nothing moves)
   B vel{}, acc_prev{};
-  if (tid < TB && il < n && steps >= 0) vel = a.vel[il];
+  if (tid < TB && il < n && steps >= 0) {
+    if (cols) {
+      vel.x = cols[4 * n + il];
+      vel.y = cols[5 * n + il];
+      vel.z = cols[6 * n + il];
+    } else {
+      vel = a.vel[il];
+    }
+  }
   const int64_t last = steps < 0 ? 0 : steps;
   for (int64_t st = 0; st <= last; ++st) {
     a.mode = steps < 0 ? NB_STEP_MODE_ACCEL
@@ -994,7 +1076,15 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
     a.pos = (st & 1) ? pos_b : pos_a;
     a.pos_next = (st & 1) ? pos_a : pos_b;
     for (int64_t j = tid; j < n; j += SN_T) {  // positions moved last step: coherent loads
-      const B b = ld4_cg(a.pos + j);
+      B b;
+      if (cols && st == 0) {
+        b.x = cols[j];
+        b.y = cols[n + j];
+        b.z = cols[2 * n + j];
+        b.w = cols[3 * n + j];
+      } else {
+        b = ld4_cg(a.pos + j);
+      }
       sp[slot(j)] = b;
       if (Core::NEEDS_LM) slm[slot(j)] = lg2_mufu((float)b.w);
     }
@@ -1044,6 +1134,15 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
 #pragma unroll
         for (int d = 0; d < 3; ++d) t[d] += red[(w * TB + tid) * 3 + d];
       integrate_body<R>(a, il, t[0], t[1], t[2], vel, acc_prev, sp[slot(il)]);
+      if (cols && st == last) {  // final state back into the columns (positions did not move in this step)
+        const B pf = sp[slot(il)];
+        cols[il] = pf.x;
+        cols[n + il] = pf.y;
+        cols[2 * n + il] = pf.z;
+        cols[4 * n + il] = vel.x;
+        cols[5 * n + il] = vel.y;
+        cols[6 * n + il] = vel.z;
+      }
     }
     if (st < steps) grid.sync();  // new positions visible; nobody still reads the old buffer, sp or red
   }
@@ -1078,22 +1177,29 @@ template <> struct Cfg<double> {
   template <bool M, bool U> using Core = CoreF64M<M, U>;
 };
 
-template <typename R, bool M, bool U, bool TMA>
+template <typename R, bool M, bool U, bool TMA, bool INFIX>
 static const void* kernel_ptr() {
   using C = Cfg<R>;
   return reinterpret_cast<const void*>(
-      &step_kernel<typename C::template Core<M, U>, C::T, C::TJ, C::MINB, NB_CHUNK, TMA>);
+      &step_kernel<typename C::template Core<M, U>, C::T, C::TJ, C::MINB, NB_CHUNK, TMA, INFIX>);
 }
 
-// The step kernel for (exclude-self, uniform-mass, TMA staging).
-template <typename R>
-static const void* step_fn(bool mask, bool uni, bool tma) {
-  if (tma) {
-    if (mask) return uni ? kernel_ptr<R, true, true, true>() : kernel_ptr<R, true, false, true>();
-    return uni ? kernel_ptr<R, false, true, true>() : kernel_ptr<R, false, false, true>();
+template <typename R, bool INFIX>
+static const void* step_fn_i(bool mask, bool uni, bool tma) {
+  if constexpr (sizeof(R) == 4) {  // (TMA staging is FP32-only)
+    if (tma) {
+      if (mask) return uni ? kernel_ptr<R, true, true, true, INFIX>() : kernel_ptr<R, true, false, true, INFIX>();
+      return uni ? kernel_ptr<R, false, true, true, INFIX>() : kernel_ptr<R, false, false, true, INFIX>();
+    }
   }
-  if (mask) return uni ? kernel_ptr<R, true, true, false>() : kernel_ptr<R, true, false, false>();
-  return uni ? kernel_ptr<R, false, true, false>() : kernel_ptr<R, false, false, false>();
+  if (mask) return uni ? kernel_ptr<R, true, true, false, INFIX>() : kernel_ptr<R, true, false, false, INFIX>();
+  return uni ? kernel_ptr<R, false, true, false, INFIX>() : kernel_ptr<R, false, false, false, INFIX>();
+}
+
+// The step kernel for (exclude-self, uniform-mass, TMA staging, in-kernel fixup).
+template <typename R>
+static const void* step_fn(bool mask, bool uni, bool tma, bool infix) {
+  return infix ? step_fn_i<R, true>(mask, uni, tma) : step_fn_i<R, false>(mask, uni, tma);
 }
 
 // TMA (bulk-copy) staging of the source tiles, FP32, launches with >=
@@ -1152,11 +1258,53 @@ static int grid_for(const void* fn, int threads) {
 template <typename R>
 int max_grid() {
   int best = 1;
-  for (int m = 0; m < 8; ++m) {
-    const int g = grid_for(step_fn<R>(m & 1, m & 2, m & 4), Cfg<R>::T);
+  for (int m = 0; m < 16; ++m) {
+    const int g = grid_for(step_fn<R>(m & 1, m & 2, m & 4, m & 8), Cfg<R>::T);
     best = g > best ? g : best;
   }
   return best;
+}
+
+// Unique, nonzero tag per launch for the slots' ready flags: a per-process
+// random salt in the high bits, a launch counter in the low ones, so a flag
+// left in a reused workspace by any earlier launch never equals a live tag.
+static unsigned long long next_tag() {
+  static std::atomic<unsigned long long> counter{0};
+  static const unsigned long long salt = [] {
+    std::random_device rd;
+    return ((unsigned long long)rd() << 32 | rd()) & 0xffffff0000000000ull;
+  }();
+  return salt | ((counter.fetch_add(1) + 1) & 0xffffffffffull);
+}
+
+// Resident CTAs per SM x SMs for a kernel (cached): the most CTAs that can be
+// co-resident, which the in-kernel fixup's waits require of the launch grid.
+static int resident_capacity(const void* fn, int threads) {
+  struct Entry { int dev; const void* fn; int cap; };
+  static Entry cache[64];
+  static int used = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  for (int k = 0; k < used; ++k)
+    if (cache[k].dev == dev && cache[k].fn == fn) return cache[k].cap;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+  const int cap = sms * per_sm;
+  if (used < 64) cache[used++] = Entry{dev, fn, cap};
+  return cap;
+}
+
+// In-kernel split-i-block fixup unless NB_FIXUP_KERNEL=1 (the separate
+// fixup_kernel launch, kept for A/B measurements and over-subscribed grids).
+static bool infix_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("NB_FIXUP_KERNEL");
+    v = (env && atoi(env) != 0) ? 0 : 1;
+  }
+  return v == 1;
 }
 
 // Host mirror of Sched::cta_of.
@@ -1175,10 +1323,24 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   constexpr int IB = C::T * C::template Core<false, false>::K;
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
-  const void* fn = step_fn<R>(mask_self, uni, tma);
+  const void* fn = step_fn<R>(mask_self, uni, tma, false);
   int grid = grid_for(fn, C::T);
   if ((int64_t)grid > g.units) grid = (int)g.units;
   a.grid = grid;
+  // Any i-block split between CTAs needs a fixup: in this launch when the grid
+  // is one resident wave, else by fixup_kernel.
+  bool split = false;
+  for (int64_t b = 0; b < g.n_iblocks && !split; ++b)
+    split = host_cta_of(b * g.n_tiles, grid, g.units) != host_cta_of(b * g.n_tiles + g.n_tiles - 1, grid, g.units);
+  bool infix = false;
+  if (split && infix_enabled()) {
+    const void* fi = step_fn<R>(mask_self, uni, tma, true);
+    if (grid <= resident_capacity(fi, C::T)) {
+      fn = fi;
+      infix = true;
+      a.tag = next_tag();
+    }
+  }
 
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1195,11 +1357,7 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   count_launch();
   if (e != cudaSuccess) return e;
 
-  // Any i-block split between CTAs needs the fixup pass.
-  bool split = false;
-  for (int64_t b = 0; b < g.n_iblocks && !split; ++b)
-    split = host_cta_of(b * g.n_tiles, grid, g.units) != host_cta_of(b * g.n_tiles + g.n_tiles - 1, grid, g.units);
-  if (split) {
+  if (split && !infix) {
     cfg.gridDim = dim3((unsigned)((a.n_i + NB_FIXUP_THREADS - 1) / NB_FIXUP_THREADS));
     cfg.blockDim = dim3(NB_FIXUP_THREADS);
     e = cudaLaunchKernelEx(&cfg, fixup_kernel<R, IB>, a);
@@ -1217,7 +1375,7 @@ cudaError_t launch_simulate_persistent(StepArgs<R> a, int flags, V4<R>* pos_a, V
   a.units = g.units;
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
-  int grid = grid_for(step_fn<R>(mask_self, uni, false), Cfg<R>::T);
+  int grid = grid_for(step_fn<R>(mask_self, uni, false, false), Cfg<R>::T);
   if ((int64_t)grid > g.units) grid = (int)g.units;
   a.grid = grid;
   int any_split = 0;
@@ -1264,7 +1422,7 @@ static const void* small_fn(bool mask_self, bool uni) {
 // 16: the measured crossovers (profiles/small_n_r01.md; NB_SMALL_PPW=4|8 forces one).
 template <typename R>
 cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b, int64_t steps,
-                                  cudaStream_t stream) {
+                                  cudaStream_t stream, R* cols) {
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
   const int64_t n = a.n_all;
@@ -1312,7 +1470,7 @@ cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>*
   const int64_t grid = (n + 2 * ppw - 1) / (2 * ppw);
   if (grid > (int64_t)capacity) return cudaErrorCooperativeLaunchTooLarge;
   int64_t L = small_split_stride(n, (SN_T / 32) * (32 / ppw));
-  void* args[] = {&a, &pos_a, &pos_b, &steps, &L};
+  void* args[] = {&a, &pos_a, &pos_b, &steps, &L, &cols};
   cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(SN_T), args, (size_t)smem, stream);
   count_launch();
   return e;
@@ -1335,11 +1493,15 @@ int64_t trace_count() {
 #endif
 
 template <typename R>
+int64_t workspace_header_bytes() {
+  return ((2 * (int64_t)max_grid<R>() * 8 + 255) / 256) * 256;
+}
+
+template <typename R>
 int64_t step_workspace_bytes(int64_t n_i) {
   const StepGeometry g = step_geometry<R>(n_i, 1);
-  const int64_t counters = counters_bytes(g.n_iblocks);
   const int64_t slots = 2 * (int64_t)max_grid<R>() * 3 * g.i_block * 8;
-  return counters + slots;
+  return workspace_header_bytes<R>() + slots;
 }
 
 template StepGeometry step_geometry<float>(int64_t, int64_t);
@@ -1350,10 +1512,13 @@ template cudaError_t launch_simulate_persistent<float>(StepArgs<float>, int, V4<
                                                       cudaStream_t);
 template cudaError_t launch_simulate_persistent<double>(StepArgs<double>, int, V4<double>*, V4<double>*, int64_t,
                                                        cudaStream_t);
+template int64_t workspace_header_bytes<float>();
+template int64_t workspace_header_bytes<double>();
 template int64_t step_workspace_bytes<float>(int64_t);
 template int64_t step_workspace_bytes<double>(int64_t);
-template cudaError_t launch_simulate_small<float>(StepArgs<float>, int, V4<float>*, V4<float>*, int64_t, cudaStream_t);
+template cudaError_t launch_simulate_small<float>(StepArgs<float>, int, V4<float>*, V4<float>*, int64_t, cudaStream_t,
+                                                  float*);
 template cudaError_t launch_simulate_small<double>(StepArgs<double>, int, V4<double>*, V4<double>*, int64_t,
-                                                   cudaStream_t);
+                                                   cudaStream_t, double*);
 
 }  // namespace nb

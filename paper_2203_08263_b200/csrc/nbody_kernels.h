@@ -31,6 +31,10 @@ struct StepArgs {
   V4<R>* vel;        // n_i
   V4<R>* pos_next;   // n_all: rows of this shard written by drift modes
   double* slots;     // stream-K partial slots (workspace)
+  // In-kernel split-i-block fixup: one ready flag per slot (workspace header),
+  // set to this launch's unique tag once the slot's partials are visible.
+  unsigned long long* flags;
+  unsigned long long tag;
   int64_t units, n_tiles, n_iblocks;
   int64_t grid;
   // Multi-GPU peer-store epilogue: the drifted rows are also stored straight
@@ -54,10 +58,13 @@ template <typename R> cudaError_t launch_simulate_persistent(StepArgs<R> a, int 
 // Small N: the whole simulate loop in one cooperative launch with the source split
 // inside each CTA (no global partials); cudaErrorCooperativeLaunchTooLarge when
 // the grid or its shared memory does not fit.
+// cols (optional): the host API's device column block, read at step 0 and
+// written with the final state (no pack/unpack launches).
 template <typename R> cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b,
-                                                        int64_t steps, cudaStream_t s);
-// Byte offset of the slot area inside the workspace (a 256-byte-aligned header).
-inline int64_t counters_bytes(int64_t n_iblocks) { return ((n_iblocks * 4 + 255) / 256) * 256; }
+                                                        int64_t steps, cudaStream_t s, R* cols = nullptr);
+// Byte offset of the slot area inside the workspace: a 256-byte-aligned header
+// holding the slots' ready flags (2 per CTA of the largest persistent grid).
+template <typename R> int64_t workspace_header_bytes();
 
 // Stand-alone O(N) kernels (nbody_update.cu).
 template <typename R> cudaError_t launch_drift(V4<R>* pos, V4<R>* vel, const V4<R>* acc, int64_t n, double dt, cudaStream_t s);

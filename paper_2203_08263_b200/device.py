@@ -154,10 +154,12 @@ class DeviceState:
         h[3 * n:4 * n] = self.masses
 
     def _staged_columns(self):
+        """Fresh host columns from the staging: ONE copy of the block, returned
+        as six contiguous 1-D views of it (positions x, y, z; owned velocities)."""
         n, ni = self.n, self.n_i
-        h = self._h_np
-        pos = tuple(np.array(h[k * n:(k + 1) * n]) for k in range(3))
-        vel = tuple(np.array(h[4 * n + k * max(ni, 1): 4 * n + k * max(ni, 1) + ni]) for k in range(3))
+        h = np.array(self._h_np)
+        pos = tuple(h[k * n:(k + 1) * n] for k in range(3))
+        vel = tuple(h[4 * n + k * max(ni, 1): 4 * n + k * max(ni, 1) + ni] for k in range(3))
         return pos, vel
 
     def simulate_columns(self, positions, velocities, masses, g: float, dt: float, eps2: float, steps: int,

@@ -79,7 +79,7 @@ def build_one(name, defs):
     os.makedirs(objdir, exist_ok=True)
     defs = dict(defs)
     extra = defs.pop("_flags", [])  # extra nvcc flags for this variant
-    dflags = [f"-D{k}={v}" for k, v in defs.items()] + list(extra)
+    dflags = [f"-D{k}={v}" for k, v in defs.items()] + list(extra) + [f'-DNB_SRC_DIGEST="{B.source_digest()}"']
     objs = []
     for src in B.SOURCES:
         o = os.path.join(objdir, src.replace(".cu", ".o"))
@@ -106,10 +106,74 @@ def build_one(name, defs):
     return name, " ".join(regs)
 
 
-def build():
+def build(only=None):
+    todo = [kv for kv in VARIANTS.items() if kv[1] is not None and (not only or kv[0] in only)]
     with ThreadPoolExecutor(8) as ex:
-        for name, info in ex.map(lambda kv: build_one(*kv), [kv for kv in VARIANTS.items() if kv[1] is not None]):
+        for name, info in ex.map(lambda kv: build_one(*kv), todo):
             print(f"{name:16s} {info}")
+
+
+def ladder_libs(rungs=None) -> dict:
+    """{rung index: path} of the ladder-rung libraries, building missing ones
+    (one nvcc run per rung, in parallel)."""
+    rungs = range(len(LADDER)) if rungs is None else rungs
+    missing = {f"ladder{i}": LADDER[i][1] for i in rungs if not os.path.exists(os.path.join(OUT, f"lib_ladder{i}.so"))}
+    if missing:
+        with ThreadPoolExecutor(8) as ex:
+            for name, info in ex.map(lambda kv: build_one(*kv), missing.items()):
+                if "FAILED" in info:
+                    raise RuntimeError(f"{name}: {info}")
+    return {i: os.path.join(OUT, f"lib_ladder{i}.so") for i in rungs}
+
+
+def variant_accel(path, st, n, eps2, mask, dtype):
+    """Accelerations of the state through one variant library's nb_dev_step (mode ACCEL)."""
+    import numpy as np
+    import torch
+    sfx = "_f32" if dtype == np.float32 else "_f64"
+    L = ctypes.CDLL(path)
+    wsb = L.nb_dev_workspace_bytes
+    wsb.restype = ctypes.c_int64
+    wsb.argtypes = [ctypes.c_int, ctypes.c_int64]
+    nbytes = wsb(np.dtype(dtype).itemsize, n)
+    ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    step = getattr(L, "nb_dev_step" + sfx)
+    step.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                     ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                     ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+    acc = torch.zeros((n, 4), dtype=st.acc.dtype, device="cuda")
+    rc = step(st.pos_a.data_ptr(), n, 0, n, 0, n, 1.0, eps2, 0.0, 0, int(mask), None, 0, acc.data_ptr(), None,
+              None, ws.data_ptr(), nbytes, 0)
+    torch.cuda.synchronize()
+    assert rc == 0, rc
+    return acc[:, :3].cpu().numpy().astype(np.float64)
+
+
+def variant_simulate(path, sys0, g, dt, eps2, steps, mask, dtype):
+    """Final positions (N, 3) of one variant library's nb_dev_simulate."""
+    import numpy as np
+    import torch
+    from paper_2203_08263_b200.device import DeviceState
+    sfx = "_f32" if dtype == np.float32 else "_f64"
+    L = ctypes.CDLL(path)
+    fn = getattr(L, "nb_dev_simulate" + sfx)
+    fn.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                                           ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]
+    wsb = L.nb_dev_workspace_bytes
+    wsb.restype = ctypes.c_int64
+    wsb.argtypes = [ctypes.c_int, ctypes.c_int64]
+    n = sys0.count
+    nbytes = wsb(np.dtype(dtype).itemsize, n)
+    ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    st = DeviceState(sys0.position_matrix().astype(dtype), np.stack(sys0.velocities, 1), sys0.masses, dtype)
+    flag = ctypes.c_int(0)
+    rc = fn(st.pos_a.data_ptr(), st.pos_b.data_ptr(), st.vel.data_ptr(), st.acc.data_ptr(), n, g, dt, eps2, steps,
+            int(mask), ws.data_ptr(), nbytes, 0, ctypes.byref(flag))
+    torch.cuda.synchronize()
+    assert rc == 0, rc
+    return (st.pos_b if flag.value else st.pos_a)[:, :3].cpu().numpy().astype(np.float64)
 
 
 def run(configs):
@@ -129,6 +193,12 @@ def run(configs):
         ref_state = DeviceState(s.position_matrix().astype(dt), np.stack(s.velocities, 1), s.masses, dt)
         mask = kernel_flags(s.masses, cfg.softening_sq, dt)
         ref_acc = ref_state.accelerations(1.0, cfg.softening_sq, mask).cpu().numpy().astype(np.float64)
+        # the oracle (long-double rows on the same rounded inputs) for every variant's accuracy
+        from oracle import oracle as O
+        rows = np.unique(np.concatenate([[0, cfg.n - 1], np.random.default_rng(3).integers(0, cfg.n, 126)]))
+        pos = s.position_matrix()
+        want = O.accel_rows_ld(*(np.ascontiguousarray(pos[:, k].astype(dt)) for k in range(3)),
+                               s.masses, rows, 1.0, cfg.softening_sq)
         only = [v for v in os.environ.get("NB_VARIANTS", "").split(",") if v]
         for name in VARIANTS:
             if only and name not in only:
@@ -163,6 +233,7 @@ def run(configs):
             torch.cuda.synchronize()
             a = acc[:, :3].cpu().numpy().astype(np.float64)
             dev = float(np.max(np.abs(a - ref_acc[:, :3]) / np.maximum(np.linalg.norm(ref_acc[:, :3], axis=1), 1e-300)[:, None]))
+            odev = O.accel_dev(a[rows], want)
 
             def sim():
                 r = fn(st.pos_a.data_ptr(), st.pos_b.data_ptr(), st.vel.data_ptr(), st.acc.data_ptr(), cfg.n, 1.0,
@@ -177,8 +248,10 @@ def run(configs):
             t = min(ts)
             rate = cfg.interactions / t
             peak = 148 * (128 if dt == np.float32 else 64) * 2 * 1.965e9
-            results[f"{cfgname}/{name}"] = {"rate": rate, "frac": 20 * rate / peak, "rc": rc, "dev_vs_base": dev}
-            print(f"{cfgname:8s} {name:16s} rate={rate:.4e} frac={20 * rate / peak:.4f} dev={dev:.2e}", flush=True)
+            results[f"{cfgname}/{name}"] = {"rate": rate, "frac": 20 * rate / peak, "rc": rc, "dev_vs_base": dev,
+                                            "accel_dev_vs_oracle": odev, "oracle_rows": int(rows.size)}
+            print(f"{cfgname:8s} {name:16s} rate={rate:.4e} frac={20 * rate / peak:.4f} dev={dev:.2e} "
+                  f"oracle_dev={odev:.2e}", flush=True)
     with open(os.path.join(REPO, "gpurun_out", "variants.json"), "w") as f:
         json.dump(results, f, indent=1)
 
@@ -188,16 +261,19 @@ def ladder_report(path):
     lines = ["# GPU optimisation ladder (FP32, C3: N=131072, 10 steps, 1 B200)", "",
              "Each rung adds one change to the previous rung; rates from `tools/variants.py run`",
              "(`nb_dev_simulate`, best of 3). Fraction = 20 flop/interaction / nominal FP32 peak.", "",
-             "| rung | interactions/s | frac of nominal FP32 | speed-up vs L0 | vs previous |",
-             "|---|---|---|---|---|"]
+             "Accuracy: `_accel_dev` (validation.py:212-225) of the rung's accelerations of the C3 initial",
+             "state against the long-double oracle on 128 sampled rows (bound 1e-5, SURVEY.md 8(c)).", "",
+             "| rung | interactions/s | frac of nominal FP32 | speed-up vs L0 | vs previous | accel_dev vs oracle |",
+             "|---|---|---|---|---|---|"]
     base = prev = None
     for i, (name, _) in enumerate(LADDER):
         r = res.get(f"C3-f32/ladder{i}")
         if r is None:
             continue
         base = base or r["rate"]
+        od = r.get("accel_dev_vs_oracle")
         lines.append(f"| {name} | {r['rate']:.3e} | {r['frac']:.3f} | {r['rate'] / base:.2f}x | "
-                     f"{(r['rate'] / prev if prev else 1.0):.2f}x |")
+                     f"{(r['rate'] / prev if prev else 1.0):.2f}x | {'—' if od is None else f'{od:.1e}'} |")
         prev = r["rate"]
     open(path, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
@@ -205,7 +281,7 @@ def ladder_report(path):
 
 if __name__ == "__main__":
     if sys.argv[1] == "build":
-        build()
+        build(sys.argv[2:] or None)
     elif sys.argv[1] == "ladder-report":
         ladder_report(sys.argv[2])
     else:
