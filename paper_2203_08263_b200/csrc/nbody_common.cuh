@@ -117,6 +117,42 @@ __device__ __forceinline__ double sq_term_f32(double e, float c) {
   return __hiloint2double((int)((f >> 3) + 0x30000000u), (int)(f << 29));
 }
 
+// Stream-K schedule over the (i-block x source chunk) units, balanced by COST:
+// a unit of a full i-block costs kg (the target groups -- pairs of target
+// bodies per thread -- it computes), a unit of the last, partial i-block only
+// lg <= kg (its dead groups are skipped: step_body's full_tile_live).  CTA c
+// owns the units whose cost positions fall in [c*cost/grid, (c+1)*cost/grid).
+// With lg == kg this is the plain equal-units split (start(c) = c*units/grid).
+struct Sched {
+  int64_t units, grid;
+  int64_t full_units;  // units of the i-blocks before the last one
+  int64_t kg, lg;      // cost of a full-i-block unit, of a last-i-block unit
+  int64_t cost;        // full_units*kg + (units - full_units)*lg
+  __host__ __device__ static Sched make(int64_t units, int64_t grid, int64_t n_tiles, int64_t n_iblocks, int64_t kg,
+                                        int64_t lg) {
+    Sched S;
+    S.units = units;
+    S.grid = grid;
+    S.full_units = (n_iblocks - 1) * n_tiles;
+    S.kg = kg;
+    S.lg = lg;
+    S.cost = S.full_units * kg + (units - S.full_units) * lg;
+    return S;
+  }
+  // cost position of the start of unit u, and the unit holding cost position x
+  __host__ __device__ __forceinline__ int64_t pos(int64_t u) const {
+    return u <= full_units ? u * kg : full_units * kg + (u - full_units) * lg;
+  }
+  __host__ __device__ __forceinline__ int64_t unit_at(int64_t x) const {
+    return x < full_units * kg ? x / kg : full_units + (x - full_units * kg) / lg;
+  }
+  __host__ __device__ __forceinline__ int64_t start(int64_t c) const { return unit_at(c * cost / grid); }
+  // CTA owning unit u: the largest c with start(c) <= u, i.e. c*cost/grid < pos(u+1).
+  __host__ __device__ __forceinline__ int64_t cta_of(int64_t u) const {
+    return (pos(u + 1) * grid + cost - 1) / cost - 1;
+  }
+};
+
 // Launch counter for the gpu_launches claim (host side).
 void count_launch(int n = 1);
 

@@ -85,6 +85,22 @@
 #ifndef NB_CHUNK
 #define NB_CHUNK 16
 #endif
+#ifndef NB_PARTIAL_GROUPS
+// 1: the last, partial i-block skips its dead target groups and the stream-K
+// schedule is balanced by cost (Sched); 0 (shipped): every unit computes all
+// groups.  Measured -10 % at C3-f32 and -9 % at C2: the two extra unrolled
+// loops push the FP32 step kernel from 248 to 255 registers and cost the
+// source loop its uniform-datapath addressing (profiles/variants_r02_infix_pg.txt).
+#define NB_PARTIAL_GROUPS 0
+#endif
+#ifndef NB_INFIX_DEFAULT
+// 1: split i-blocks are finished inside the step kernel (ready flags); 0
+// (shipped): by fixup_kernel.  NB_FIXUP_KERNEL=0/1 in the environment overrides
+// at run time.  Measured -3 % at C3-f32 and -8 % at C2: with the fixup code
+// after the source loop ptxas schedules the loop worse (general-register
+// addressing, +6 MOVs per 16 sources; profiles/variants_r02_infix_pg.txt).
+#define NB_INFIX_DEFAULT 0
+#endif
 #ifndef NB_FIXUP_THREADS
 // Threads per fixup CTA (one split body each).  Small CTAs spread the
 // latency-bound fixup over every SM: C2 +1.7 % against 256-thread CTAs
@@ -164,15 +180,10 @@ __device__ __forceinline__ void trace_rec(int tag, unsigned long long t_entry, u
 #define NB_TRACE_END(tag) do { } while (0)
 #endif
 
-struct Sched {
-  int64_t units;
-  int64_t grid;
-  __device__ __forceinline__ int64_t start(int64_t c) const { return c * units / grid; }
-  // CTA owning unit u: the largest c with start(c) <= u.
-  __device__ __forceinline__ int64_t cta_of(int64_t u) const {
-    return ((u + 1) * grid + units - 1) / units - 1;
-  }
-};
+template <typename R>
+__host__ __device__ __forceinline__ Sched sched_of(const StepArgs<R>& a) {
+  return Sched::make(a.units, a.grid, a.n_tiles, a.n_iblocks, a.sched_kg, a.sched_lg);
+}
 
 // ---------------------------------------------------------------- packed FP32x2
 // Two FP32 lanes in one 64-bit register (lo = first body, hi = second).  The
@@ -360,14 +371,19 @@ struct CoreF32 {
     return w;
   }
 
-  __device__ __forceinline__ void interact(const F4& pj, int jj) {
+  static constexpr int KG = KP;  // target groups (pairs) per thread
+  __device__ __forceinline__ void interact(const F4& pj, int jj) { interact_g<KP>(pj, jj); }
+  // One source body against the first NG target pairs (the rest are dead rows
+  // of a partial i-block: skipped).
+  template <int NG>
+  __device__ __forceinline__ void interact_g(const F4& pj, int jj) {
     const f2x xj = pk(pj.x, pj.x), yj = pk(pj.y, pj.y), zj = pk(pj.z, pj.z), mj = pk(pj.w, pj.w);
     float lm = 0.f;
     if (NEEDS_LM) lm = lmt[jj];
     const f2x lmj = pk(lm, lm);
 #if !NB_F32_STAGEWISE
 #pragma unroll
-    for (int q = 0; q < KP; ++q) {  // ladder rung: per-pair order
+    for (int q = 0; q < NG; ++q) {  // ladder rung: per-pair order
       const f2x dx = add2(xj, nx[q]), dy = add2(yj, ny[q]), dz = add2(zj, nz[q]);
       f2x d2 = fma2(dx, dx, e2);
       d2 = fma2(dy, dy, d2);
@@ -378,36 +394,36 @@ struct CoreF32 {
       tz[q] = fma2(dz, w, tz[q]);
     }
 #else
-    f2x dx[KP], dy[KP], dz[KP], d2[KP], w[KP];
+    f2x dx[NG], dy[NG], dz[NG], d2[NG], w[NG];
 #pragma unroll
-    for (int q = 0; q < KP; ++q) dx[q] = add2(xj, nx[q]);
+    for (int q = 0; q < NG; ++q) dx[q] = add2(xj, nx[q]);
 #pragma unroll
-    for (int q = 0; q < KP; ++q) dy[q] = add2(yj, ny[q]);
+    for (int q = 0; q < NG; ++q) dy[q] = add2(yj, ny[q]);
 #pragma unroll
-    for (int q = 0; q < KP; ++q) dz[q] = add2(zj, nz[q]);
+    for (int q = 0; q < NG; ++q) dz[q] = add2(zj, nz[q]);
 #pragma unroll
-    for (int q = 0; q < KP; ++q) d2[q] = fma2(dx[q], dx[q], e2);
+    for (int q = 0; q < NG; ++q) d2[q] = fma2(dx[q], dx[q], e2);
 #pragma unroll
-    for (int q = 0; q < KP; ++q) d2[q] = fma2(dy[q], dy[q], d2[q]);
+    for (int q = 0; q < NG; ++q) d2[q] = fma2(dy[q], dy[q], d2[q]);
 #pragma unroll
-    for (int q = 0; q < KP; ++q) d2[q] = fma2(dz[q], dz[q], d2[q]);
+    for (int q = 0; q < NG; ++q) d2[q] = fma2(dz[q], dz[q], d2[q]);
 #pragma unroll
-    for (int q = 0; q < KP; ++q) w[q] = weight(d2[q], mj, lmj, jj, q);
+    for (int q = 0; q < NG; ++q) w[q] = weight(d2[q], mj, lmj, jj, q);
 #pragma unroll
-    for (int q = 0; q < KP; ++q) {
+    for (int q = 0; q < NG; ++q) {
       tx[q] = fma2(w[q], dx[q], tx[q]);
       ty[q] = fma2(w[q], dy[q], ty[q]);
       tz[q] = fma2(w[q], dz[q], tz[q]);
     }
 #endif
   }
-  // A full tile of TJ source bodies, unrolled UNROLL_ deep.  (Software-
-  // pipelining stage A of body j+1 against stage B of body j was measured
-  // slower: profiles/variants_r01_sweep2.txt, "pipe".)
-  template <int TJ>
+  // A full tile of TJ source bodies against the first NG pairs, unrolled
+  // UNROLL_ deep.  (Software-pipelining stage A of body j+1 against stage B of
+  // body j was measured slower: profiles/variants_r01_sweep2.txt, "pipe".)
+  template <int TJ, int NG = KP>
   __device__ __forceinline__ void full_tile(const F4* tb) {
 #pragma unroll UNROLL_
-    for (int jj = 0; jj < TJ; ++jj) interact(tile_get<TJ>(tb, jj), jj);
+    for (int jj = 0; jj < TJ; ++jj) interact_g<NG>(tile_get<TJ>(tb, jj), jj);
   }
   __device__ __forceinline__ void end_tile() {
 #pragma unroll
@@ -454,30 +470,36 @@ struct CoreF64 {
   }
   __device__ __forceinline__ void begin_tile() {}
   __device__ __forceinline__ void end_tile() {}
-  template <int TJ>
+  static constexpr int KG = K / 2;  // target groups (pairs) per thread, as in the FP32 core
+  template <int TJ, int NG = KG>
   __device__ __forceinline__ void full_tile(const D4* tb) {
 #pragma unroll UNROLL_
-    for (int jj = 0; jj < TJ; ++jj) interact(tile_get<TJ>(tb, jj), jj);
+    for (int jj = 0; jj < TJ; ++jj) interact_g<NG>(tile_get<TJ>(tb, jj), jj);
   }
-  __device__ __forceinline__ void interact(const D4& pj, int jj) {
+  __device__ __forceinline__ void interact(const D4& pj, int jj) { interact_g<KG>(pj, jj); }
+  // One source body against the first 2*NG targets (the rest are dead rows of a
+  // partial i-block: skipped).
+  template <int NG>
+  __device__ __forceinline__ void interact_g(const D4& pj, int jj) {
+    constexpr int NK = 2 * NG;
 #if NB_F64_STAGEWISE
     // Stage-wise across the K targets with w in the first slot of the
     // accumulating DFMAs (the FP32 kernel's measured best source form).
-    double dx[K], dy[K], dz[K], d2[K], w[K];
+    double dx[NK], dy[NK], dz[NK], d2[NK], w[NK];
 #pragma unroll
-    for (int k = 0; k < K; ++k) dx[k] = pj.x + nx[k];
+    for (int k = 0; k < NK; ++k) dx[k] = pj.x + nx[k];
 #pragma unroll
-    for (int k = 0; k < K; ++k) dy[k] = pj.y + ny[k];
+    for (int k = 0; k < NK; ++k) dy[k] = pj.y + ny[k];
 #pragma unroll
-    for (int k = 0; k < K; ++k) dz[k] = pj.z + nz[k];
+    for (int k = 0; k < NK; ++k) dz[k] = pj.z + nz[k];
 #pragma unroll
-    for (int k = 0; k < K; ++k) d2[k] = fma(dx[k], dx[k], e2);
+    for (int k = 0; k < NK; ++k) d2[k] = fma(dx[k], dx[k], e2);
 #pragma unroll
-    for (int k = 0; k < K; ++k) d2[k] = fma(dy[k], dy[k], d2[k]);
+    for (int k = 0; k < NK; ++k) d2[k] = fma(dy[k], dy[k], d2[k]);
 #pragma unroll
-    for (int k = 0; k < K; ++k) d2[k] = fma(dz[k], dz[k], d2[k]);
+    for (int k = 0; k < NK; ++k) d2[k] = fma(dz[k], dz[k], d2[k]);
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < NK; ++k) {
       const double y = rsqrt_seed(d2[k]);
       const double t = y * y;
       const double e = fma(-d2[k], t, 1.0);
@@ -487,14 +509,14 @@ struct CoreF64 {
       if (MASK && jj == selfj[k]) w[k] = 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < NK; ++k) {
       sx[k] = fma(w[k], dx[k], sx[k]);
       sy[k] = fma(w[k], dy[k], sy[k]);
       sz[k] = fma(w[k], dz[k], sz[k]);
     }
 #else
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < NK; ++k) {
       const double dx = pj.x + nx[k], dy = pj.y + ny[k], dz = pj.z + nz[k];
       double d2 = fma(dx, dx, e2);
       d2 = fma(dy, dy, d2);
@@ -622,6 +644,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// Full source tile against the ng live target groups of this i-block: the
+// group count selects one of KG unrolled loops (a uniform branch outside the
+// source loop), so a partial last i-block skips its dead rows' arithmetic.
+template <class Core, int TJ, int NG>
+__device__ __forceinline__ void full_tile_live(Core& core, const V4<typename Core::R>* tb, int ng) {
+  if constexpr (NG > 1) {
+    if (ng < NG) {
+      full_tile_live<Core, TJ, NG - 1>(core, tb, ng);
+      return;
+    }
+  }
+  core.template full_tile<TJ, NG>(tb);
+}
+
 // ---------------------------------------------------------------- split i-block fixup
 // Ready flags of the partial slots (in-kernel fixup): a slot's flag holds the
 // launch's unique tag once its partials are visible at GPU scope.
@@ -645,12 +681,12 @@ __device__ __forceinline__ int64_t slot_of(const Sched& S, int64_t NT, int64_t b
 // CTAs cf..cl summed in ascending CTA order (L2 loads: other CTAs of this or an
 // earlier launch wrote them), then the epilogue.
 template <typename R, int IB>
-__device__ __forceinline__ void fixup_one(const StepArgs<R>& a, const Sched& S, int64_t b, int64_t o, int64_t cf,
+__device__ __forceinline__ void fixup_one(const StepArgs<R>& a, int64_t slot_cf, int64_t b, int64_t o, int64_t cf,
                                           int64_t cl) {
   const int64_t il = b * IB + o;
   double tx = 0.0, ty = 0.0, tz = 0.0;
   for (int64_t cc = cf; cc <= cl; ++cc) {
-    const int64_t sl = slot_of(S, a.n_tiles, b, cf, cc);
+    const int64_t sl = cc == cf ? slot_cf : 2 * cc;
     NB_DCHECK(sl >= 0 && sl < 2 * a.grid && cc < a.grid && o < IB);
     const double* q = a.slots + sl * 3 * IB + o;
     tx += __ldcg(q);
@@ -658,6 +694,57 @@ __device__ __forceinline__ void fixup_one(const StepArgs<R>& a, const Sched& S, 
     tz += __ldcg(q + 2 * IB);
   }
   finalize_body<R>(a, il, tx, ty, tz);
+}
+
+// In-kernel fixup plan of a CTA (INFIX, see step_body): for the split
+// i-blocks it contributed to -- the ones holding its first and its last unit --
+// the i-block, its first and last contributing CTAs and the first one's slot.
+// Computed in the kernel's prologue next to the schedule's other divisions; the
+// code after the source loop then has none (with the 64-bit divisions there,
+// ptxas gave the source loop worse code: general instead of uniform-datapath
+// addressing, -3 % at C3).
+struct FixPlan {
+  long long b[2], cf[2], cl[2], slot_cf[2];
+};
+
+__device__ __forceinline__ void make_fix_plan(FixPlan& p, const Sched& S, int64_t NT, int64_t c) {
+  const int64_t u_begin = S.start(c), u_end = S.start(c + 1);
+  const int64_t bb[2] = {u_begin / NT, (u_end - 1) / NT};
+  for (int k = 0; k < 2; ++k) {
+    const int64_t b = bb[k];
+    const int64_t cf = S.cta_of(b * NT), cl = S.cta_of(b * NT + NT - 1);
+    const bool use = u_end > u_begin && cf != cl && !(k == 1 && bb[1] == bb[0]);
+    p.b[k] = use ? b : -1;
+    p.cf[k] = cf;
+    p.cl[k] = cl;
+    p.slot_cf[k] = slot_of(S, NT, b, cf, cf);
+  }
+}
+
+// Wait for every contributor's ready flag, then finish this CTA's 1/m share of
+// the i-block's bodies (m contributors).
+template <typename R, int T, int IB>
+__device__ __forceinline__ void infix_fixup(const StepArgs<R>& a, const FixPlan& p) {
+  const int tid = threadIdx.x;
+  const int64_t c = blockIdx.x;
+  for (int k = 0; k < 2; ++k) {
+    const int64_t b = p.b[k];
+    if (b < 0) continue;
+    const int64_t cf = p.cf[k], cl = p.cl[k];
+    if (tid < 32) {  // warp 0: one lane per contributor polls its slot's flag
+      for (int64_t cc = cf + tid; cc <= cl; cc += 32) {
+        const unsigned long long* f = a.flags + (cc == cf ? p.slot_cf[k] : 2 * cc);
+        while (flag_load(f) != a.tag) __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    const int64_t m = cl - cf + 1, r = c - cf;
+    const int64_t rows = min((int64_t)IB, a.n_i - b * IB);
+    // (r+1)*rows/m with rows <= IB and m <= grid: 32-bit division suffices
+    const int64_t o0 = (int64_t)((uint32_t)(r * rows) / (uint32_t)m);
+    const int64_t o1 = (int64_t)((uint32_t)((r + 1) * rows) / (uint32_t)m);
+    for (int64_t o = o0 + tid; o < o1; o += T) fixup_one<R, IB>(a, p.slot_cf[k], b, o, cf, cl);
+  }
 }
 
 // One force(+update) pass of the stream-K decomposition: the body of
@@ -687,10 +774,14 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
 
   const int tid = threadIdx.x;
   const int64_t c = blockIdx.x;
-  const Sched S{a.units, a.grid};
+  const Sched S = sched_of(a);
   const int64_t NT = a.n_tiles;  // source chunks of CH bodies per i-block
   const int64_t u_begin = S.start(c), u_end = S.start(c + 1);
 
+  __shared__ long long s_plan[INFIX ? sizeof(FixPlan) / 8 : 1];
+  if constexpr (INFIX) {
+    if (tid == 0) make_fix_plan(*reinterpret_cast<FixPlan*>(s_plan), S, NT, c);
+  }
   Core core;
   core.init(a.eps2, s_sums + tid, T);
   uint32_t phase_bits = 0u;  // mbarrier phase parity of tile buffer b in bit b (TMA staging)
@@ -702,6 +793,10 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
     const int64_t t1 = min(NT, t0 + (u_end - u));
     // this segment's source offsets [s0, s1) within the j range
     const int64_t s0 = t0 * CH, s1 = min(t1 * CH, a.j_count);
+#if NB_PARTIAL_GROUPS
+    // live target groups: all but in the last, partial i-block
+    const int ng = b == a.n_iblocks - 1 ? a.sched_lg : Core::KG;
+#endif
 #if NB_TRACE
     unsigned long long tseg[5];
     tseg[0] = gtimer();
@@ -795,7 +890,11 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
       core.lmt = tile_lm[buf];
       const B* tb = tile[buf];
       if (count == TJ) {
+#if NB_PARTIAL_GROUPS
+        full_tile_live<Core, TJ, Core::KG>(core, tb, ng);
+#else
         core.template full_tile<TJ>(tb);
+#endif
       } else {
         int jj = 0;
 #pragma unroll 1
@@ -854,25 +953,8 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
     u += t1 - t0;
   }
   if constexpr (INFIX) {
-    // The split i-blocks this CTA contributed to hold its first and its last unit.
-    const int64_t bf = u_begin / NT, bl = (u_end - 1) / NT;
-    for (int pass = 0; pass < 2 && u_end > u_begin; ++pass) {
-      const int64_t b = pass == 0 ? bf : bl;
-      if (pass == 1 && bl == bf) break;
-      const int64_t cf = S.cta_of(b * NT), cl = S.cta_of(b * NT + NT - 1);
-      if (cf == cl) continue;  // finished whole by its one CTA
-      if (tid < 32) {  // warp 0: one lane per contributor polls its slot's flag
-        for (int64_t cc = cf + tid; cc <= cl; cc += 32) {
-          const unsigned long long* f = a.flags + slot_of(S, NT, b, cf, cc);
-          while (flag_load(f) != a.tag) __nanosleep(64);
-        }
-      }
-      __syncthreads();
-      const int64_t m = cl - cf + 1, r = c - cf;
-      const int64_t rows = min((int64_t)IB, a.n_i - b * IB);
-      const int64_t o1 = (r + 1) * rows / m;
-      for (int64_t o = r * rows / m + tid; o < o1; o += T) fixup_one<R, IB>(a, S, b, o, cf, cl);
-    }
+    __syncthreads();
+    infix_fixup<R, T, IB>(a, *reinterpret_cast<const FixPlan*>(s_plan));
   }
   if (a.n_peers) __threadfence_system();  // peer stores visible before the rank barrier
 }
@@ -923,12 +1005,12 @@ __global__ void __launch_bounds__(NB_FIXUP_THREADS) fixup_kernel(const StepArgs<
 template <typename R, int IB>
 __device__ __forceinline__ void fixup_body(const StepArgs<R>& a, int64_t il) {
   if (il >= a.n_i) return;
-  const Sched S{a.units, a.grid};
+  const Sched S = sched_of(a);
   const int64_t NT = a.n_tiles;
   const int64_t b = il / IB, o = il - b * IB;
   const int64_t cf = S.cta_of(b * NT), cl = S.cta_of(b * NT + NT - 1);
   if (cf == cl) return;
-  fixup_one<R, IB>(a, S, b, o, cf, cl);
+  fixup_one<R, IB>(a, slot_of(S, NT, b, cf, cf), b, o, cf, cl);
 }
 
 // ---------------------------------------------------------------- persistent multi-step kernel
@@ -1302,14 +1384,44 @@ static bool infix_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* env = getenv("NB_FIXUP_KERNEL");
-    v = (env && atoi(env) != 0) ? 0 : 1;
+    v = env ? (atoi(env) != 0 ? 0 : 1) : NB_INFIX_DEFAULT;
   }
   return v == 1;
 }
 
-// Host mirror of Sched::cta_of.
-static inline int64_t host_cta_of(int64_t u, int64_t grid, int64_t units) {
-  return ((u + 1) * grid + units - 1) / units - 1;
+// Cost-balanced schedule parameters of a launch (Sched): the live target
+// groups of the last i-block (NB_FULL_GROUPS=1 computes every group there, the
+// plain equal-units split, for A/B measurements).
+template <typename R>
+static void set_sched(StepArgs<R>& a, const StepGeometry& g) {
+  constexpr int KG = Cfg<R>::template Core<false, false>::KG;
+  static int full = -1;
+  if (full < 0) {
+    const char* env = getenv("NB_FULL_GROUPS");
+    full = (env && atoi(env) != 0) ? 1 : 0;
+  }
+  const int64_t rows_last = a.n_i - (g.n_iblocks - 1) * (int64_t)g.i_block;
+  const int64_t live = (rows_last + 2 * (int64_t)g.threads - 1) / (2 * (int64_t)g.threads);
+  a.sched_kg = KG;
+  a.sched_lg = (full || !NB_PARTIAL_GROUPS) ? KG : (int)(live < 1 ? 1 : (live > KG ? KG : live));
+}
+
+// The persistent grid capped so every CTA owns at least one unit: a CTA's cost
+// share must be >= the most expensive unit (cost / grid >= kg).
+template <typename R>
+static int capped_grid(const StepArgs<R>& a, int grid) {
+  const int64_t cost = Sched::make(a.units, 1, a.n_tiles, a.n_iblocks, a.sched_kg, a.sched_lg).cost;
+  const int64_t cap = cost / a.sched_kg;
+  return (int)(grid < cap ? grid : (cap < 1 ? 1 : cap));
+}
+
+// Any i-block whose units are split between CTAs (needs a fixup).
+template <typename R>
+static bool any_split_iblock(const StepArgs<R>& a) {
+  const Sched S = sched_of(a);
+  for (int64_t b = 0; b < a.n_iblocks; ++b)
+    if (S.cta_of(b * a.n_tiles) != S.cta_of(b * a.n_tiles + a.n_tiles - 1)) return true;
+  return false;
 }
 
 template <typename R>
@@ -1318,20 +1430,18 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   a.n_tiles = g.n_tiles;
   a.n_iblocks = g.n_iblocks;
   a.units = g.units;
+  set_sched<R>(a, g);
   const bool tma = use_tma<R>(a.n_i, a.j_count);
   using C = Cfg<R>;
   constexpr int IB = C::T * C::template Core<false, false>::K;
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
   const void* fn = step_fn<R>(mask_self, uni, tma, false);
-  int grid = grid_for(fn, C::T);
-  if ((int64_t)grid > g.units) grid = (int)g.units;
+  const int grid = capped_grid<R>(a, grid_for(fn, C::T));
   a.grid = grid;
   // Any i-block split between CTAs needs a fixup: in this launch when the grid
   // is one resident wave, else by fixup_kernel.
-  bool split = false;
-  for (int64_t b = 0; b < g.n_iblocks && !split; ++b)
-    split = host_cta_of(b * g.n_tiles, grid, g.units) != host_cta_of(b * g.n_tiles + g.n_tiles - 1, grid, g.units);
+  const bool split = any_split_iblock<R>(a);
   bool infix = false;
   if (split && infix_enabled()) {
     const void* fi = step_fn<R>(mask_self, uni, tma, true);
@@ -1373,14 +1483,12 @@ cudaError_t launch_simulate_persistent(StepArgs<R> a, int flags, V4<R>* pos_a, V
   a.n_tiles = g.n_tiles;
   a.n_iblocks = g.n_iblocks;
   a.units = g.units;
+  set_sched<R>(a, g);
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
-  int grid = grid_for(step_fn<R>(mask_self, uni, false, false), Cfg<R>::T);
-  if ((int64_t)grid > g.units) grid = (int)g.units;
+  const int grid = capped_grid<R>(a, grid_for(step_fn<R>(mask_self, uni, false, false), Cfg<R>::T));
   a.grid = grid;
-  int any_split = 0;
-  for (int64_t b = 0; b < g.n_iblocks && !any_split; ++b)
-    any_split = host_cta_of(b * g.n_tiles, grid, g.units) != host_cta_of(b * g.n_tiles + g.n_tiles - 1, grid, g.units);
+  int any_split = any_split_iblock<R>(a) ? 1 : 0;
   using C = Cfg<R>;
   void* args[] = {&a, &pos_a, &pos_b, &steps, &any_split};
   const void* fn;

@@ -37,6 +37,9 @@ struct StepArgs {
   unsigned long long tag;
   int64_t units, n_tiles, n_iblocks;
   int64_t grid;
+  // Cost-balanced stream-K (Sched in nbody_force.cu): target groups per thread
+  // of a full i-block, and the live ones of the last (partial) i-block.
+  int sched_kg, sched_lg;
   // Multi-GPU peer-store epilogue: the drifted rows are also stored straight
   // into every peer GPU's next-position buffer over NVLink (no all-gather).
   V4<R>* peers[kMaxPeers];

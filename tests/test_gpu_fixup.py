@@ -1,6 +1,7 @@
 """The split-i-block fixup inside the step kernel (ready flags per partial slot,
-each contributor finishing its share; the default) against the separate
-fixup_kernel launch (NB_FIXUP_KERNEL=1): the same partial sums in the same
+each contributor finishing its share; NB_FIXUP_KERNEL=0 -- an opt-in variant,
+measured slower) against the separate fixup_kernel launch (the shipped
+default, NB_FIXUP_KERNEL=1): the same partial sums in the same
 ascending CTA order, so the trajectories must be bitwise identical -- at the
 C2 size (11 i-blocks over 148 CTAs: every i-block split), FP64, a ragged N, a
 sharded two-phase (carry) step and the uniform-mass path."""
@@ -42,10 +43,7 @@ SCRIPT = textwrap.dedent(f"""
 
 
 def _run(path, fixup_kernel):
-    env = dict(os.environ)
-    env.pop("NB_FIXUP_KERNEL", None)
-    if fixup_kernel:
-        env["NB_FIXUP_KERNEL"] = "1"
+    env = dict(os.environ, NB_FIXUP_KERNEL="1" if fixup_kernel else "0")
     r = subprocess.run([sys.executable, "-c", SCRIPT, str(path)], capture_output=True, text=True, timeout=600,
                        env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]

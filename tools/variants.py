@@ -45,6 +45,12 @@ VARIANTS = {
     "k4_p3": {"NB_F32_K": 4, "NB_F32_EXP2_MASK": 9, "NB_F32_EXP2_PHASES": 3},
     "k4_p4_3of8": {"NB_F32_K": 4, "NB_F32_EXP2_MASK": 25, "NB_F32_EXP2_PHASES": 4},
     "k4_p4_2of8": {"NB_F32_K": 4, "NB_F32_EXP2_MASK": 33, "NB_F32_EXP2_PHASES": 4},
+    # round 2: split-i-block fixup in the step kernel (INFIX) and the partial last
+    # i-block's dead-group skipping with the cost-balanced schedule (PG), each on/off
+    "pg0_fixk": {"NB_PARTIAL_GROUPS": 0, "NB_INFIX_DEFAULT": 0},
+    "pg0_infix": {"NB_PARTIAL_GROUPS": 0, "NB_INFIX_DEFAULT": 1},
+    "pg1_fixk": {"NB_PARTIAL_GROUPS": 1, "NB_INFIX_DEFAULT": 0},
+    "pg1_infix": {"NB_PARTIAL_GROUPS": 1, "NB_INFIX_DEFAULT": 1},
     # extra nvcc flags per variant: {"_flags": ["-Xptxas", "..."]}
 }
 
