@@ -67,6 +67,9 @@ extern "C" {
 #define NB_FLAG_UNIFORM_MASS 2 /* caller guarantees every m_j equals pos4[0].w: terms omit
                                   m_j and the sum is scaled by m once (one FMUL2 less per
                                   interaction pair)                                          */
+#define NB_FLAG_AUTO 256       /* nb_dev_simulate_cols_* only: derive the two flags above
+                                  from the host mass column itself (one pass over n masses
+                                  in C, instead of the caller's)                            */
 
 /* ---------------------------------------------------------------- host (FFI mirror) */
 

@@ -24,6 +24,7 @@ NB_STEP_KICK_DRIFT = 2
 NB_STEP_FINAL_KICK = 3
 NB_FLAG_EXCLUDE_SELF = 1
 NB_FLAG_UNIFORM_MASS = 2
+NB_FLAG_AUTO = 256  # nb_dev_simulate_cols_*: flags derived from the staged masses in C
 NB_INIT_UNIFORM_CUBE = 0
 NB_INIT_PLUMMER = 1
 

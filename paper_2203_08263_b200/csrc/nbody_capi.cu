@@ -593,6 +593,9 @@ int dev_simulate_cols(const void* host_cols, void* dev_cols, void* pos_a, void* 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   R* d = static_cast<R*>(dev_cols);
   NB_CUDA(cudaMemcpyAsync(d, host_cols, (size_t)(7 * n) * sizeof(R), cudaMemcpyHostToDevice, st));
+  if (flags & NB_FLAG_AUTO)  // (while the copy runs) the flags of the staged masses
+    flags = (flags & ~(NB_FLAG_AUTO | NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS)) |
+            host_flags<R>(static_cast<const R*>(host_cols) + 3 * n, n, eps2);
   int in_b = 0, done = 0;
   int rc = dev_simulate<R>(pos_a, pos_b, vel4, acc4, n, g, dt, eps2, steps, flags, ws, ws_bytes, stream, &in_b,
                            nullptr, d, &done);

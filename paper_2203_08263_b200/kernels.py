@@ -329,16 +329,17 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
         _store(state, "velocities", vel)
         return state
     # Single GPU: columns go straight into the pinned column staging of the
-    # resident state (one H2D, packed on the device) and the result columns come
-    # back unpacked on the device in one D2H.
-    from .device import kernel_flags
+    # resident state (one H2D; at small N the simulate kernel reads and writes
+    # the columns itself) and the result columns come back in one D2H; the
+    # kernel flags are derived from the staged masses inside the native call.
+    from ._native import NB_FLAG_AUTO
     m = np.asarray(sys_.masses, dtype)
     with _STATE_LOCK:
         pc, vc = _columns(sys_, "positions"), _columns(sys_, "velocities")
         st = _resident_state(pc, vc, m, dtype, load=False)
         # upload, simulate and read back in one native call (nb_dev_simulate_cols)
         pos, vel = st.simulate_columns(pc, vc, m, params.gravitational_constant, params.dt, params.softening_sq,
-                                       params.steps, kernel_flags(m, params.softening_sq, dtype))
+                                       params.steps, NB_FLAG_AUTO)
     if _value(sys_.layout) != "soa":
         pos, vel = np.stack(pos, 1), np.stack(vel, 1)
     return type(sys_)(sys_.layout, sys_.precision, pos, vel, sys_.masses.copy())

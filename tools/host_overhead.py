@@ -43,3 +43,9 @@ t("st.columns_host (syncs)", lambda: st.columns_host())
 t("d_cols.copy_(h_cols) H2D + sync", lambda: st._d_cols.copy_(st._h_cols, non_blocking=True), sync=True)
 t("h_cols.copy_(d_cols) D2H (syncs)", lambda: st._h_cols.copy_(st._d_cols))
 t("nb.simulate end to end", lambda: nb.simulate(s, p))
+pc, vc = K._columns(s, "positions"), K._columns(s, "velocities")
+t("st._fill_staging (python)", lambda: st._fill_staging(pc, vc, m))
+t("st._staged_columns (python)", lambda: st._staged_columns())
+t("st.simulate_columns (one native call, syncs)",
+  lambda: st.simulate_columns(pc, vc, m, 1.0, p.dt, p.softening_sq, p.steps, _native.NB_FLAG_AUTO))
+t("nb.simulate end to end (again)", lambda: nb.simulate(s, p))
