@@ -359,6 +359,9 @@ def run_ours(args) -> dict:
     dev = torch.device("cuda", local_dev)
     if world > 1:
         if backend == "nccl":
+            # NCCL's communicator log (stderr) shows every rank joining
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
@@ -514,7 +517,7 @@ def run_ours(args) -> dict:
     e2e = None
     if not args.no_e2e:
         sys_host = cfg.system()
-        for _ in range(min(args.warmup, 2)):
+        for _ in range(args.warmup):
             nb.simulate(sys_host, params)
         torch.cuda.synchronize()
         barrier()
@@ -529,11 +532,12 @@ def run_ours(args) -> dict:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         # Bytes each simulate() moves (whole job): N=1 uploads the column block
-        # x, y, z, m, vx, vy, vz (7 N) and reads back x, y, z, vx, vy, vz (6 N);
-        # a sharded rank uploads x, y, z, m of all padded bodies plus its own
-        # velocity rows and reads back all N positions and velocities.
+        # x, y, z, m, vx, vy, vz (7 N) and reads the same block back (one copy:
+        # the result columns plus the unchanged masses); a sharded rank uploads
+        # x, y, z, m of all padded bodies plus its own velocity rows and reads
+        # back all N positions and velocities.
         if world == 1:
-            h2d, d2h = 7 * cfg.n * pbytes, 6 * cfg.n * pbytes
+            h2d, d2h = 7 * cfg.n * pbytes, 7 * cfg.n * pbytes
         else:
             h2d = world * (4 * npad + 3 * ni) * pbytes
             d2h = world * 6 * cfg.n * pbytes

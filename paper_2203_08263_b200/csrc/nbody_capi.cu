@@ -172,7 +172,8 @@ int dev_step(const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int6
 template <typename R>
 int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, double g, double dt,
                  double eps2, int64_t steps, int flags, void* ws, int64_t ws_bytes, void* stream,
-                 int* final_in_b, cudaEvent_t* events = nullptr, R* cols = nullptr, int* cols_done = nullptr) {
+                 int* final_in_b, cudaEvent_t* events = nullptr, R* cols = nullptr, int* cols_done = nullptr,
+                 R* cols_out = nullptr) {
   if (steps < 1) return fail(NB_ERR_ARG, "steps must be >= 1");
   if (!(dt > 0.0)) return fail(NB_ERR_ARG, "dt must be positive");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -186,10 +187,10 @@ int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, do
     if (rc == 0) {
       cudaError_t e = launch_simulate_small<R>(a, flags & (NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS),
                                                static_cast<V4<R>*>(pos_a), static_cast<V4<R>*>(pos_b), steps, st,
-                                               cols);
+                                               cols, cols_out);
       if (e == cudaSuccess) {
         if (final_in_b) *final_in_b = (steps & 1) ? 1 : 0;
-        if (cols_done) *cols_done = cols ? 1 : 0;
+        if (cols_done) *cols_done = cols ? (cols_out ? 2 : 1) : 0;
         return NB_OK;
       }
       if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported)
@@ -596,9 +597,17 @@ int dev_simulate_cols(const void* host_cols, void* dev_cols, void* pos_a, void* 
   if (flags & NB_FLAG_AUTO)  // (while the copy runs) the flags of the staged masses
     flags = (flags & ~(NB_FLAG_AUTO | NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS)) |
             host_flags<R>(static_cast<const R*>(host_cols) + 3 * n, n, eps2);
+  // A pinned host block is mapped into the device's address space (UVA): the
+  // small-N kernel then stores the final columns straight into it, and no D2H
+  // copy follows (done == 2).
+  R* hdev = nullptr;
+  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), const_cast<void*>(host_cols), 0) != cudaSuccess) {
+    cudaGetLastError();
+    hdev = nullptr;
+  }
   int in_b = 0, done = 0;
   int rc = dev_simulate<R>(pos_a, pos_b, vel4, acc4, n, g, dt, eps2, steps, flags, ws, ws_bytes, stream, &in_b,
-                           nullptr, d, &done);
+                           nullptr, d, &done, hdev);
   if (rc) return rc;
   if (final_in_b) *final_in_b = in_b;
   if (!done) {
@@ -607,7 +616,9 @@ int dev_simulate_cols(const void* host_cols, void* dev_cols, void* pos_a, void* 
   }
   // one D2H of the whole block (the masses ride along unchanged: one copy's
   // latency instead of two at small N)
-  NB_CUDA(cudaMemcpyAsync(const_cast<void*>(host_cols), d, (size_t)(7 * n) * sizeof(R), cudaMemcpyDeviceToHost, st));
+  if (done != 2)
+    NB_CUDA(cudaMemcpyAsync(const_cast<void*>(host_cols), d, (size_t)(7 * n) * sizeof(R), cudaMemcpyDeviceToHost,
+                            st));
   NB_CUDA(cudaStreamSynchronize(st));
   return NB_OK;
 }

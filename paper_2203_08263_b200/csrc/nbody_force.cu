@@ -547,7 +547,7 @@ template <typename R>
 __device__ __forceinline__ void integrate_body(const StepArgs<R>& a, int64_t il, double tx, double ty, double tz,
                                                V4<R>& v, V4<R>& ap, V4<R> p) {
   // Uniform-mass kernels left m_j out of every term: apply it once here.
-  const double gm = a.uniform_mass ? a.g * (double)a.pos[0].w : a.g;
+  const double gm = a.uniform_mass ? a.g * (double)(a.mass0 ? *a.mass0 : a.pos[0].w) : a.g;
   const R ax = (R)(tx * gm), ay = (R)(ty * gm), az = (R)(tz * gm);
   V4<R> an;
   an.x = ax; an.y = ay; an.z = az; an.w = R(0);
@@ -1102,7 +1102,8 @@ template <class Core, int PPW>
 __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename Core::R> a,
                                                               V4<typename Core::R>* pos_a,
                                                               V4<typename Core::R>* pos_b, int64_t steps,
-                                                              int64_t L, typename Core::R* cols) {
+                                                              int64_t L, typename Core::R* cols,
+                                                              typename Core::R* cols_out) {
   using R = typename Core::R;
   using B = V4<R>;
   constexpr int G = 32 / PPW;        // lane groups per warp
@@ -1157,6 +1158,8 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
                        : (st == 0 ? NB_STEP_MODE_FIRST : (st < steps ? NB_STEP_MODE_KICK_DRIFT : NB_STEP_MODE_FINAL));
     a.pos = (st & 1) ? pos_b : pos_a;
     a.pos_next = (st & 1) ? pos_a : pos_b;
+    // step 0 of a column-block run: the packed buffer holds no state yet
+    a.mass0 = (cols && st == 0) ? cols + 3 * n : nullptr;
     for (int64_t j = tid; j < n; j += SN_T) {  // positions moved last step: coherent loads
       B b;
       if (cols && st == 0) {
@@ -1218,12 +1221,13 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
       integrate_body<R>(a, il, t[0], t[1], t[2], vel, acc_prev, sp[slot(il)]);
       if (cols && st == last) {  // final state back into the columns (positions did not move in this step)
         const B pf = sp[slot(il)];
-        cols[il] = pf.x;
-        cols[n + il] = pf.y;
-        cols[2 * n + il] = pf.z;
-        cols[4 * n + il] = vel.x;
-        cols[5 * n + il] = vel.y;
-        cols[6 * n + il] = vel.z;
+        R* co = cols_out ? cols_out : cols;
+        co[il] = pf.x;
+        co[n + il] = pf.y;
+        co[2 * n + il] = pf.z;
+        co[4 * n + il] = vel.x;
+        co[5 * n + il] = vel.y;
+        co[6 * n + il] = vel.z;
       }
     }
     if (st < steps) grid.sync();  // new positions visible; nobody still reads the old buffer, sp or red
@@ -1530,7 +1534,7 @@ static const void* small_fn(bool mask_self, bool uni) {
 // 16: the measured crossovers (profiles/small_n_r01.md; NB_SMALL_PPW=4|8 forces one).
 template <typename R>
 cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b, int64_t steps,
-                                  cudaStream_t stream, R* cols) {
+                                  cudaStream_t stream, R* cols, R* cols_out) {
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
   const int64_t n = a.n_all;
@@ -1578,7 +1582,7 @@ cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>*
   const int64_t grid = (n + 2 * ppw - 1) / (2 * ppw);
   if (grid > (int64_t)capacity) return cudaErrorCooperativeLaunchTooLarge;
   int64_t L = small_split_stride(n, (SN_T / 32) * (32 / ppw));
-  void* args[] = {&a, &pos_a, &pos_b, &steps, &L, &cols};
+  void* args[] = {&a, &pos_a, &pos_b, &steps, &L, &cols, &cols_out};
   cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(SN_T), args, (size_t)smem, stream);
   count_launch();
   return e;
@@ -1625,8 +1629,8 @@ template int64_t workspace_header_bytes<double>();
 template int64_t step_workspace_bytes<float>(int64_t);
 template int64_t step_workspace_bytes<double>(int64_t);
 template cudaError_t launch_simulate_small<float>(StepArgs<float>, int, V4<float>*, V4<float>*, int64_t, cudaStream_t,
-                                                  float*);
+                                                  float*, float*);
 template cudaError_t launch_simulate_small<double>(StepArgs<double>, int, V4<double>*, V4<double>*, int64_t,
-                                                   cudaStream_t, double*);
+                                                   cudaStream_t, double*, double*);
 
 }  // namespace nb

@@ -26,6 +26,7 @@ struct StepArgs {
   R dt, half, f;     // (R)dt, (R)0.5, (R)(0.5*dt)  (_accel_cy.pyx:211-212; __init__.py:223)
   int mode, carry_mode;
   int uniform_mass;  // 1: every m_j equals pos[0].w; terms omit m_j, the sum is scaled once
+  const R* mass0;    // where that mass is read instead of pos[0].w (nullptr: pos[0].w)
   double* carry;     // 3*n_i FP64 partial sums (SoA), carry_mode 1/2
   V4<R>* acc;        // n_i: a_prev in, a out
   V4<R>* vel;        // n_i
@@ -62,9 +63,12 @@ template <typename R> cudaError_t launch_simulate_persistent(StepArgs<R> a, int 
 // inside each CTA (no global partials); cudaErrorCooperativeLaunchTooLarge when
 // the grid or its shared memory does not fit.
 // cols (optional): the host API's device column block, read at step 0 and
-// written with the final state (no pack/unpack launches).
+// written with the final state (no pack/unpack launches); cols_out (optional):
+// where the final state goes instead -- the device view of the caller's
+// pinned host block, so no D2H copy follows.
 template <typename R> cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b,
-                                                        int64_t steps, cudaStream_t s, R* cols = nullptr);
+                                                        int64_t steps, cudaStream_t s, R* cols = nullptr,
+                                                        R* cols_out = nullptr);
 // Byte offset of the slot area inside the workspace: a 256-byte-aligned header
 // holding the slots' ready flags (2 per CTA of the largest persistent grid).
 template <typename R> int64_t workspace_header_bytes();
