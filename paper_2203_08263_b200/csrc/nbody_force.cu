@@ -1343,11 +1343,21 @@ static int grid_for(const void* fn, int threads) {
 // (sizes the stream-K slot workspace).
 template <typename R>
 int max_grid() {
+  // Cached per device (every step launch sizes its workspace with it: at small
+  // N the host side of a launch is on simulate()'s critical path).
+  static std::atomic<int> cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c > 0) return c;
+  }
   int best = 1;
   for (int m = 0; m < 16; ++m) {
     const int g = grid_for(step_fn<R>(m & 1, m & 2, m & 4, m & 8), Cfg<R>::T);
     best = g > best ? g : best;
   }
+  if (dev >= 0 && dev < 64) cache[dev].store(best, std::memory_order_relaxed);
   return best;
 }
 
