@@ -101,12 +101,6 @@
 // addressing, +6 MOVs per 16 sources; profiles/variants_r02_infix_pg.txt).
 #define NB_INFIX_DEFAULT 0
 #endif
-#ifndef NB_CHUNKED_PARTIAL
-// 1: the partial last tile of a stream-K segment runs the UNROLL-deep loop body
-// in chunks (its length is a multiple of the chunk CH except at the end of the
-// j range); 0: a 4-deep rolled loop.
-#define NB_CHUNKED_PARTIAL 0
-#endif
 #ifndef NB_FIXUP_THREADS
 // Threads per fixup CTA (one split body each).  Small CTAs spread the
 // latency-bound fixup over every SM: C2 +1.7 % against 256-thread CTAs
@@ -339,12 +333,12 @@ struct CoreF32 {
   // order): consecutive instructions share the broadcast source operand, and the
   // accumulate -- the instruction with three distinct register pairs, which the
   // register file cannot feed at full rate -- gets the most reuse.
-  __device__ __forceinline__ f2x weight(f2x d2, f2x mj, f2x lmj, int jj, int ph, int q) const {
+  __device__ __forceinline__ f2x weight(f2x d2, f2x mj, f2x lmj, int jj, int q) const {
     float d2a, d2b;
     upk(d2, d2a, d2b);
     f2x w;
 #if NB_F32_MATH == 0
-    if ((XMASK >> (q + KP * (ph % NB_F32_EXP2_PHASES))) & 1u) {
+    if ((XMASK >> (q + KP * (jj % NB_F32_EXP2_PHASES))) & 1u) {
       // m d2^(-3/2) = 2^(-1.5 log2 d2 + log2 m): one FFMA2 and four MUFU ops in
       // place of three FMUL2 + two MUFU.RSQ -- moves FP32-pipe work onto the XU
       // pipe, which the rsqrt form leaves ~40 % idle.
@@ -378,13 +372,11 @@ struct CoreF32 {
   }
 
   static constexpr int KG = KP;  // target groups (pairs) per thread
-  __device__ __forceinline__ void interact(const F4& pj, int jj) { interact_g<KP>(pj, jj, jj); }
+  __device__ __forceinline__ void interact(const F4& pj, int jj) { interact_g<KP>(pj, jj); }
   // One source body against the first NG target pairs (the rest are dead rows
   // of a partial i-block: skipped).
-  // ph: jj or any value congruent to it mod NB_F32_EXP2_PHASES known at compile
-  // time (the LG2/EX2 weights are chosen by source phase).
   template <int NG>
-  __device__ __forceinline__ void interact_g(const F4& pj, int jj, int ph) {
+  __device__ __forceinline__ void interact_g(const F4& pj, int jj) {
     const f2x xj = pk(pj.x, pj.x), yj = pk(pj.y, pj.y), zj = pk(pj.z, pj.z), mj = pk(pj.w, pj.w);
     float lm = 0.f;
     if (NEEDS_LM) lm = lmt[jj];
@@ -396,7 +388,7 @@ struct CoreF32 {
       f2x d2 = fma2(dx, dx, e2);
       d2 = fma2(dy, dy, d2);
       d2 = fma2(dz, dz, d2);
-      const f2x w = weight(d2, mj, lmj, jj, ph, q);
+      const f2x w = weight(d2, mj, lmj, jj, q);
       tx[q] = fma2(dx, w, tx[q]);
       ty[q] = fma2(dy, w, ty[q]);
       tz[q] = fma2(dz, w, tz[q]);
@@ -416,7 +408,7 @@ struct CoreF32 {
 #pragma unroll
     for (int q = 0; q < NG; ++q) d2[q] = fma2(dz[q], dz[q], d2[q]);
 #pragma unroll
-    for (int q = 0; q < NG; ++q) w[q] = weight(d2[q], mj, lmj, jj, ph, q);
+    for (int q = 0; q < NG; ++q) w[q] = weight(d2[q], mj, lmj, jj, q);
 #pragma unroll
     for (int q = 0; q < NG; ++q) {
       tx[q] = fma2(w[q], dx[q], tx[q]);
@@ -431,18 +423,7 @@ struct CoreF32 {
   template <int TJ, int NG = KP>
   __device__ __forceinline__ void full_tile(const F4* tb) {
 #pragma unroll UNROLL_
-    for (int jj = 0; jj < TJ; ++jj) interact_g<NG>(tile_get<TJ>(tb, jj), jj, jj);
-  }
-  // The first cnt (a multiple of UNROLL_) bodies of a partial tile, in the same
-  // UNROLL_-deep body as full_tile (the source phase of j0 + u is u's).
-  static constexpr int UNROLL = UNROLL_;
-  template <int TJ>
-  __device__ __forceinline__ void part_tile(const F4* tb, int cnt) {
-#pragma unroll 1
-    for (int j0 = 0; j0 < cnt; j0 += UNROLL_) {
-#pragma unroll
-      for (int u = 0; u < UNROLL_; ++u) interact_g<KP>(tile_get<TJ>(tb, j0 + u), j0 + u, u);
-    }
+    for (int jj = 0; jj < TJ; ++jj) interact_g<NG>(tile_get<TJ>(tb, jj), jj);
   }
   __device__ __forceinline__ void end_tile() {
 #pragma unroll
@@ -494,15 +475,6 @@ struct CoreF64 {
   __device__ __forceinline__ void full_tile(const D4* tb) {
 #pragma unroll UNROLL_
     for (int jj = 0; jj < TJ; ++jj) interact_g<NG>(tile_get<TJ>(tb, jj), jj);
-  }
-  static constexpr int UNROLL = UNROLL_;
-  template <int TJ>
-  __device__ __forceinline__ void part_tile(const D4* tb, int cnt) {
-#pragma unroll 1
-    for (int j0 = 0; j0 < cnt; j0 += UNROLL_) {
-#pragma unroll
-      for (int u = 0; u < UNROLL_; ++u) interact_g<KG>(tile_get<TJ>(tb, j0 + u), j0 + u);
-    }
   }
   __device__ __forceinline__ void interact(const D4& pj, int jj) { interact_g<KG>(pj, jj); }
   // One source body against the first 2*NG targets (the rest are dead rows of a
@@ -925,12 +897,6 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
 #endif
       } else {
         int jj = 0;
-#if NB_CHUNKED_PARTIAL
-        // stream-K segments end on CH-body chunk boundaries: all but the tail of
-        // the j range runs the unrolled body
-        jj = count & ~(Core::UNROLL - 1);
-        core.template part_tile<TJ>(tb, jj);
-#endif
 #pragma unroll 1
         for (; jj + 4 <= count; jj += 4) {
           core.interact(tile_get<TJ>(tb, jj), jj);

@@ -51,10 +51,6 @@ VARIANTS = {
     "pg0_infix": {"NB_PARTIAL_GROUPS": 0, "NB_INFIX_DEFAULT": 1},
     "pg1_fixk": {"NB_PARTIAL_GROUPS": 1, "NB_INFIX_DEFAULT": 0},
     "pg1_infix": {"NB_PARTIAL_GROUPS": 1, "NB_INFIX_DEFAULT": 1},
-    # round 2: partial segment tiles through the unrolled body in chunks; batched fixup loads
-    "chunk": {"NB_CHUNKED_PARTIAL": 1},
-    "fixb8": {"NB_FIXUP_BATCH": 8},
-    "chunk_fixb8": {"NB_CHUNKED_PARTIAL": 1, "NB_FIXUP_BATCH": 8},
     # extra nvcc flags per variant: {"_flags": ["-Xptxas", "..."]}
 }
 
