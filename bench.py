@@ -277,7 +277,7 @@ def measure_traffic(args, single_launch: bool) -> dict:
     committed ncu summary (profiles/ncu_summary.json) when ncu is unavailable."""
     if args.no_traffic or not os.path.exists(NCU):
         return {"traffic": load_traffic(args.config), "traffic_source": "profiles/ncu_summary.json (committed capture)"}
-    kname = "regex:small_simulate_kernel|simulate_kernel" if single_launch else "regex:step_kernel"
+    kname = "regex:small_simulate_kernel|simulate_kernel" if single_launch else "regex:step_kernel|pair_kernel"
     cmd = [NCU, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none",
            "-k", kname, "--launch-skip", "1", "-c", "1", "--csv", "--print-units", "base",
            sys.executable, os.path.abspath(__file__), "--traffic-child", args.config]
@@ -480,6 +480,9 @@ def run_ours(args) -> dict:
     peak = nominal_peak_tflops(pbytes)
     launches_per_sim = launches / max(1, args.steps)
     kernel_name = "nb::step_kernel (fused force + velocity-Verlet epilogue) + nb::fixup_kernel"
+    if world == 1 and _native.step_kernel_name(pbytes, cfg.n, cfg.n) == "pair_kernel":
+        kernel_name = ("nb::pair_kernel (2-CTA cluster split-source force + velocity-Verlet epilogue; "
+                       "no fixup launch)")
     launch_timing = ("CUDA events between consecutive launches on the launch stream "
                      "(nb_dev_simulate_timed), one simulate right after the timed steps")
     single_launch = world == 1 and launches_per_sim == 1
@@ -502,7 +505,7 @@ def run_ours(args) -> dict:
         mean_launch_s = statistics.mean(step_ms) / 1e3 / (steps + 1)
         achieved = FLOP_PER_INTERACTION * float(cfg.n) * cfg.n / mean_launch_s / 1e12
         launch_timing = ("CUDA events around each timed simulate on its launch stream / its steps+1 step "
-                         "launches (each with its fixup launch; PDL overlap intact)")
+                         "launches (with their fixup launches where stream-K splits i-blocks; PDL overlap intact)")
     else:
         mean_launch_s = total_s / (args.steps * (steps + 1))
         achieved = FLOP_PER_INTERACTION * interactions / total_s / 1e12 / world

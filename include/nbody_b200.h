@@ -120,6 +120,14 @@ int nb_host_simulate_soa_f64(double* px, double* py, double* pz, double* vx, dou
  * between CTAs): no initialisation needed, reusable across calls on one stream. */
 int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i);
 
+/* Name of the force kernel a nb_dev_step_* launch of n_i targets against
+ * j_count sources runs on the current device: "pair_kernel" (FP32 launches
+ * whose 224-target i-blocks fill one wave of 2-CTA clusters -- the source range
+ * split over 16 warps and reduced through distributed shared memory) or
+ * "step_kernel" (stream-K + split-i-block fixup).  Diagnostic (bench, tests);
+ * NULL on a bad precision. */
+const char* nb_dev_step_kernel(int precision_bytes, int64_t n_i, int64_t j_count);
+
 /* Fused softened all-pairs force (+ optional velocity-Verlet update) for the
  * target rows [i_begin, i_begin+n_i) of pos4 (n_all bodies) against the source
  * bodies j in [j_begin, j_begin+j_count) taken modulo n_all (circular, so a

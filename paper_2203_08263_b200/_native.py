@@ -84,6 +84,8 @@ def lib() -> ctypes.CDLL:
                 fn.restype = _i
         L.nb_dev_workspace_bytes.argtypes = [_i, _i64]
         L.nb_dev_workspace_bytes.restype = _i64
+        L.nb_dev_step_kernel.argtypes = [_i, _i64, _i64]
+        L.nb_dev_step_kernel.restype = ctypes.c_char_p
         L.nb_energy_workspace_bytes.argtypes = [_i, _i64]
         L.nb_energy_workspace_bytes.restype = _i64
         L.nb_comm_unique_id.argtypes = [_p]
@@ -146,6 +148,11 @@ def energy_workspace_bytes(precision_bytes: int, n: int) -> int:
 
 def workspace_bytes(precision_bytes: int, n_i: int) -> int:
     return int(lib().nb_dev_workspace_bytes(precision_bytes, n_i))
+
+
+def step_kernel_name(precision_bytes: int, n_i: int, j_count: int) -> str:
+    """The force kernel nb_dev_step runs for this launch shape (current device)."""
+    return lib().nb_dev_step_kernel(precision_bytes, n_i, j_count).decode()
 
 
 def launch_count() -> int:

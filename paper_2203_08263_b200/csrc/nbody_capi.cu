@@ -720,6 +720,13 @@ int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i) {
   return -1;
 }
 
+const char* nb_dev_step_kernel(int precision_bytes, int64_t n_i, int64_t j_count) {
+  if (precision_bytes == 4) return step_kernel_name<float>(n_i, j_count);
+  if (precision_bytes == 8) return step_kernel_name<double>(n_i, j_count);
+  fail(NB_ERR_ARG, "precision_bytes must be 4 or 8");
+  return nullptr;
+}
+
 int64_t nb_energy_workspace_bytes(int precision_bytes, int64_t n) {
   if (n < 1) n = 1;
   if (precision_bytes != 4 && precision_bytes != 8) {

@@ -101,6 +101,9 @@
 // addressing, +6 MOVs per 16 sources; profiles/variants_r02_infix_pg.txt).
 #define NB_INFIX_DEFAULT 0
 #endif
+#ifndef NB_PAIR_ODD_FIRST
+#define NB_PAIR_ODD_FIRST 0  // pair_kernel: the odd target's source pair before (1) or after (0) the pairs'
+#endif
 #ifndef NB_FIXUP_THREADS
 // Threads per fixup CTA (one split body each).  Small CTAs spread the
 // latency-bound fixup over every SM: C2 +1.7 % against 256-thread CTAs
@@ -281,6 +284,9 @@ struct CoreF32 {
   using R = float;
   static constexpr int K = K_;
   static constexpr int KP = K / 2;
+  // Odd K (the cluster kernel's 7 targets per thread): the last target runs as
+  // one scalar FP32 lane beside the KP packed pairs, always in the rsqrt form.
+  static constexpr bool ODD = (K & 1) != 0;
   static constexpr unsigned XMASK = NB_F32_EXP2_MASK & ((1u << (NB_F32_EXP2_PHASES * KP)) - 1u);  // LG2/EX2 weights
   static constexpr bool NEEDS_LM = XMASK != 0 && !UNI;  // needs log2(m_j) per source
   const float* lmt;  // this tile's log2(m_j) (NEEDS_LM)
@@ -292,13 +298,24 @@ struct CoreF32 {
 #endif
   f2x nx[KP], ny[KP], nz[KP];  // negated target positions, paired
   f2x tx[KP], ty[KP], tz[KP];  // FP32 partial sums of the current tile
+  float onx, ony, onz;          // ODD: the scalar target's negated position
+  float otx, oty, otz;          // ODD: its FP32 partial sums of the current tile
+  // ODD, full tiles: the odd target runs packed over source PAIRS (2p, 2p+1)
+  // read from a pair-interleaved copy of the tile, tbi[2p] = (x0,x1,y0,y1),
+  // tbi[2p+1] = (z0,z1,m0,m1): the same packed FFMA2/FADD2/FMUL2 stream per
+  // interaction as the target pairs (a scalar lane costs twice the issue slots).
+  const float4* tbi;
+  f2x pnx, pny, pnz;            // the odd target's negated position, broadcast
+  f2x ptx, pty, ptz;            // its FP32 partials: even / odd sources of the tile
   int selfj[K];
   f2x e2;
+  float e2s;
   double* ss;  // this thread's FP64 sums: ss[(d*K + k) * stride]
   int stride;
 
   __device__ __forceinline__ void init(float eps2, double* s, int st) {
     e2 = pk(eps2, eps2);
+    e2s = eps2;
     ss = s;
     stride = st;
   }
@@ -309,6 +326,38 @@ struct CoreF32 {
     nx[q] = add2(0ull, pk(-p0.x, -p1.x));
     ny[q] = add2(0ull, pk(-p0.y, -p1.y));
     nz[q] = add2(0ull, pk(-p0.z, -p1.z));
+  }
+  __device__ __forceinline__ void set_single(const F4& p) {  // ODD: target K-1
+    onx = -p.x;
+    ony = -p.y;
+    onz = -p.z;
+    pnx = add2(0ull, pk(-p.x, -p.x));
+    pny = add2(0ull, pk(-p.y, -p.y));
+    pnz = add2(0ull, pk(-p.z, -p.z));
+  }
+  // The odd target against source pair (2p, 2p+1) of the interleaved tile
+  // (a, b = tbi[2p], tbi[2p+1]).
+  __device__ __forceinline__ void interact_odd2(const float4& a, const float4& b, int p) {
+    const f2x xs = pk(a.x, a.y), ys = pk(a.z, a.w), zs = pk(b.x, b.y), ms = pk(b.z, b.w);
+    const f2x dx = add2(xs, pnx), dy = add2(ys, pny), dz = add2(zs, pnz);
+    f2x d2 = fma2(dx, dx, e2);
+    d2 = fma2(dy, dy, d2);
+    d2 = fma2(dz, dz, d2);
+    float d2a, d2b;
+    upk(d2, d2a, d2b);
+    const f2x r = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
+    const f2x r2 = mul2(r, r);
+    f2x w = UNI ? mul2(r2, r) : mul2(mul2(r, ms), r2);
+    if (MASK) {
+      float wa, wb;
+      upk(w, wa, wb);
+      if (2 * p == selfj[K - 1]) wa = 0.f;
+      if (2 * p + 1 == selfj[K - 1]) wb = 0.f;
+      w = pk(wa, wb);
+    }
+    ptx = fma2(w, dx, ptx);
+    pty = fma2(w, dy, pty);
+    ptz = fma2(w, dz, ptz);
   }
 #if NB_F32_SUMS_IN_REGS
   __device__ __forceinline__ double& acc_ref(int i) { return rs[i]; }
@@ -326,6 +375,10 @@ struct CoreF32 {
   __device__ __forceinline__ void begin_tile() {
 #pragma unroll
     for (int q = 0; q < KP; ++q) tx[q] = ty[q] = tz[q] = 0ull;
+    if constexpr (ODD) {
+      otx = oty = otz = 0.f;
+      ptx = pty = ptz = 0ull;
+    }
   }
   // One source body against the K targets.  Written stage-wise across the KP
   // pairs with w in the first operand slot of the accumulating FFMA2s: the
@@ -375,7 +428,7 @@ struct CoreF32 {
   __device__ __forceinline__ void interact(const F4& pj, int jj) { interact_g<KP>(pj, jj); }
   // One source body against the first NG target pairs (the rest are dead rows
   // of a partial i-block: skipped).
-  template <int NG>
+  template <int NG, bool SCALAR_ODD = true>
   __device__ __forceinline__ void interact_g(const F4& pj, int jj) {
     const f2x xj = pk(pj.x, pj.x), yj = pk(pj.y, pj.y), zj = pk(pj.z, pj.z), mj = pk(pj.w, pj.w);
     float lm = 0.f;
@@ -416,14 +469,40 @@ struct CoreF32 {
       tz[q] = fma2(w[q], dz[q], tz[q]);
     }
 #endif
+    if constexpr (ODD && SCALAR_ODD && NG == KP) {
+      const float dxs = __fadd_rn(pj.x, onx), dys = __fadd_rn(pj.y, ony), dzs = __fadd_rn(pj.z, onz);
+      float d2s = __fmaf_rn(dxs, dxs, e2s);
+      d2s = __fmaf_rn(dys, dys, d2s);
+      d2s = __fmaf_rn(dzs, dzs, d2s);
+      const float r = rsqrt_mufu(d2s);
+      const float r2 = __fmul_rn(r, r);
+      float ws = UNI ? __fmul_rn(r2, r) : __fmul_rn(__fmul_rn(r, pj.w), r2);
+      if (MASK && jj == selfj[K - 1]) ws = 0.f;
+      otx = __fmaf_rn(ws, dxs, otx);
+      oty = __fmaf_rn(ws, dys, oty);
+      otz = __fmaf_rn(ws, dzs, otz);
+    }
   }
   // A full tile of TJ source bodies against the first NG pairs, unrolled
   // UNROLL_ deep.  (Software-pipelining stage A of body j+1 against stage B of
   // body j was measured slower: profiles/variants_r01_sweep2.txt, "pipe".)
   template <int TJ, int NG = KP>
   __device__ __forceinline__ void full_tile(const F4* tb) {
+    if constexpr (ODD && NG == KP) {
+      // every source read from the pair-interleaved tile (tbi): the pairs'
+      // broadcast bodies and the odd target's packed source pair alike
+#pragma unroll UNROLL_ / 2
+      for (int p = 0; p < TJ / 2; ++p) {
+        const float4 a = tbi[2 * p], b = tbi[2 * p + 1];
+        if (NB_PAIR_ODD_FIRST) interact_odd2(a, b, p);
+        interact_g<NG, false>(F4{a.x, a.z, b.x, b.z}, 2 * p);
+        interact_g<NG, false>(F4{a.y, a.w, b.y, b.w}, 2 * p + 1);
+        if (!NB_PAIR_ODD_FIRST) interact_odd2(a, b, p);
+      }
+    } else {
 #pragma unroll UNROLL_
-    for (int jj = 0; jj < TJ; ++jj) interact_g<NG>(tile_get<TJ>(tb, jj), jj);
+      for (int jj = 0; jj < TJ; ++jj) interact_g<NG>(tile_get<TJ>(tb, jj), jj);
+    }
   }
   __device__ __forceinline__ void end_tile() {
 #pragma unroll
@@ -438,6 +517,15 @@ struct CoreF32 {
       upk(tz[q], a, b);
       acc_ref(2 * K + 2 * q) += (double)a;
       acc_ref(2 * K + 2 * q + 1) += (double)b;
+    }
+    if constexpr (ODD) {
+      float ea, eb;
+      upk(ptx, ea, eb);
+      acc_ref(0 * K + K - 1) += (double)otx + ((double)ea + (double)eb);
+      upk(pty, ea, eb);
+      acc_ref(1 * K + K - 1) += (double)oty + ((double)ea + (double)eb);
+      upk(ptz, ea, eb);
+      acc_ref(2 * K + K - 1) += (double)otz + ((double)ea + (double)eb);
     }
   }
 };
@@ -982,6 +1070,182 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
   NB_TRACE_END(1);
 }
 
+// ---------------------------------------------------------------- cluster split-source kernel
+// Mid-size FP32 launches (C2: N = 16384; the per-rank size of C3 at 8 GPUs).
+// Stream-K there splits every i-block between ~14 CTAs, and the FP64 partial
+// slots, the fixup launch and the two kernel boundaries around it cost ~10 % of
+// a 116 us step (profiles/trace_C2_r01.md).  This kernel splits the SOURCES
+// instead, inside a 2-CTA cluster: cluster c owns i-block c of IBC = 32*K
+// targets (every warp holds all of them, K per lane), and each of its 16 warps
+// runs one 1/16 slice of the source range out of its own double-buffered tiles
+// (cp.async.bulk on a per-warp mbarrier: no CTA-wide barrier in the loop).  The
+// 16 slice sums of a target are then added in fixed slice order, the peer
+// CTA's through distributed shared memory, and CTA r runs the epilogue of half
+// r of the i-block: no partial slots, no fixup launch, bitwise reproducible.
+// With 74 clusters on 148 SMs, K = 7 covers N <= 16576 (C2: 1.2 % dead lanes).
+#ifndef NB_PAIR_K
+#define NB_PAIR_K 7
+#endif
+#ifndef NB_PAIR_TJ
+#define NB_PAIR_TJ 256
+#endif
+#ifndef NB_PAIR_UNROLL
+#define NB_PAIR_UNROLL 32
+#endif
+constexpr int PR_T = 256;             // threads per CTA
+constexpr int PR_W = PR_T / 32;       // warps = source slices per CTA
+constexpr int PR_CL = 2;              // CTAs per cluster
+constexpr int PR_S = PR_W * PR_CL;    // source slices per i-block
+
+template <bool M, bool U> struct CorePair : CoreF32<NB_PAIR_K, M, NB_PAIR_UNROLL, U> {
+  static constexpr bool MASK_SELF = M;
+};
+
+template <class Core, int TJ>
+constexpr int64_t pair_smem_bytes() {
+  return (int64_t)PR_W * 3 * TJ * sizeof(F4) + (Core::NEEDS_LM ? (int64_t)PR_W * 2 * TJ * 4 : 0) +
+         (int64_t)3 * Core::K * PR_T * 8 + PR_W * 2 * 8;
+}
+
+template <class Core, int TJ>
+__global__ void __cluster_dims__(PR_CL, 1, 1) __launch_bounds__(PR_T, 1) pair_kernel(const StepArgs<float> a) {
+  using B = F4;
+  constexpr int K = Core::K;
+  constexpr int IBC = 32 * K;
+  extern __shared__ __align__(128) unsigned char pr_smem[];
+  B* tiles = reinterpret_cast<B*>(pr_smem);                                        // [warp][2][TJ]
+  float4* ilv = reinterpret_cast<float4*>(tiles + PR_W * 2 * TJ);                  // [warp][TJ] interleaved
+  float* lms = reinterpret_cast<float*>(ilv + PR_W * TJ);                          // [warp][2][TJ] (NEEDS_LM)
+  double* sums = reinterpret_cast<double*>(lms + (Core::NEEDS_LM ? PR_W * 2 * TJ : 0));  // [3K][PR_T]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sums + 3 * K * PR_T);               // [warp][2]
+  cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)cluster.block_rank();
+  const int64_t blk = blockIdx.x / PR_CL;
+  // this warp's slice [s0, s1) of the j range (multiples of 16 bodies but the end)
+  const int64_t per = (a.j_count + PR_S * 16 - 1) / (PR_S * 16) * 16;
+  const int sl = rank * PR_W + warp;
+  const int64_t s0 = min(a.j_count, sl * per), s1 = min(a.j_count, s0 + per);
+  B* tw = tiles + warp * 2 * TJ;
+  float* lw = lms + warp * 2 * TJ;
+  uint64_t* bw = bars + warp * 2;
+  if (lane == 0) {
+    mbar_init(bw, 1);
+    mbar_init(bw + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  NB_TRACE_ENTRY();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  NB_TRACE_WAITED();
+  asm volatile("griddepcontrol.launch_dependents;");
+
+  Core core;
+  core.init(a.eps2, sums + tid, PR_T);
+#pragma unroll
+  for (int q = 0; q < K / 2; ++q) {
+    const int64_t i0 = blk * IBC + (2 * q) * 32 + lane, i1 = i0 + 32;
+    core.set_pair(q, ld4(a.pos + a.i_begin + (i0 < a.n_i ? i0 : a.n_i - 1)),
+                  ld4(a.pos + a.i_begin + (i1 < a.n_i ? i1 : a.n_i - 1)));
+  }
+  if constexpr (Core::ODD) {
+    const int64_t i0 = blk * IBC + (K - 1) * 32 + lane;
+    core.set_single(ld4(a.pos + a.i_begin + (i0 < a.n_i ? i0 : a.n_i - 1)));
+  }
+  core.zero_sums();
+
+  // lane 0 arms the buffer's mbarrier and issues the tile (two copies when the
+  // circular source range wraps); the warp waits on the buffer's phase
+  auto issue = [&](int buf, int64_t lo) {
+    if (lane == 0) {
+      const int64_t cnt = min((int64_t)TJ, s1 - lo);
+      int64_t jg = a.j_begin + lo;
+      if (jg >= a.n_all) jg -= a.n_all;
+      const int64_t n1 = min(cnt, a.n_all - jg);
+      mbar_expect_tx(bw + buf, (uint32_t)(cnt * sizeof(B)));
+      bulk_g2s(tw + buf * TJ, a.pos + jg, (uint32_t)(n1 * sizeof(B)), bw + buf);
+      if (cnt > n1) bulk_g2s(tw + buf * TJ + n1, a.pos, (uint32_t)((cnt - n1) * sizeof(B)), bw + buf);
+    }
+  };
+  uint32_t phase_bits = 0u;
+  if (s0 < s1) issue(0, s0);
+  int buf = 0;
+  for (int64_t lo = s0; lo < s1; lo += TJ) {
+    const bool more = lo + TJ < s1;
+    mbar_wait(bw + buf, (phase_bits >> buf) & 1u);
+    phase_bits ^= 1u << buf;
+    if (more) issue(buf ^ 1, lo + TJ);  // buf^1 was released by the __syncwarp below
+    const B* tb = tw + buf * TJ;
+    const int count = (int)min((int64_t)TJ, s1 - lo);
+    if (Core::NEEDS_LM) {
+      for (int r = lane; r < count; r += 32) lw[buf * TJ + r] = lg2_mufu(tb[r].w);
+      __syncwarp();
+    }
+    if (Core::MASK_SELF) {
+      int64_t base = a.j_begin + lo;
+      if (base >= a.n_all) base -= a.n_all;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        int64_t rel = a.i_begin + blk * IBC + k * 32 + lane - base;
+        if (rel < 0) rel += a.n_all;
+        core.selfj[k] = rel < count ? (int)rel : -1;
+      }
+    }
+    core.begin_tile();
+    core.lmt = lw + buf * TJ;
+    if (count == TJ) {
+      if constexpr (Core::ODD) {  // pair-interleaved copy of the tile for the odd target
+        float4* ti = ilv + warp * TJ;
+#pragma unroll
+        for (int p = lane; p < TJ / 2; p += 32) {
+          const B b0 = tb[2 * p], b1 = tb[2 * p + 1];
+          ti[2 * p] = make_float4(b0.x, b1.x, b0.y, b1.y);
+          ti[2 * p + 1] = make_float4(b0.z, b1.z, b0.w, b1.w);
+        }
+        __syncwarp();
+        core.tbi = ti;
+      }
+      core.template full_tile<TJ>(tb);
+    } else {
+      int jj = 0;
+#pragma unroll 1
+      for (; jj + 4 <= count; jj += 4) {
+        core.interact(tb[jj], jj);
+        core.interact(tb[jj + 1], jj + 1);
+        core.interact(tb[jj + 2], jj + 2);
+        core.interact(tb[jj + 3], jj + 3);
+      }
+#pragma unroll 1
+      for (; jj < count; ++jj) core.interact(tb[jj], jj);
+    }
+    core.end_tile();
+    buf ^= 1;
+    __syncwarp();
+  }
+
+  // every slice's FP64 sums (in shared memory) visible to both CTAs
+  cluster.sync();
+  // CTA r: targets [r*IBC/2, (r+1)*IBC/2) of the i-block; slice order 0..15
+  const double* part[PR_CL];
+#pragma unroll
+  for (int r = 0; r < PR_CL; ++r) part[r] = cluster.map_shared_rank(sums, r);
+  for (int t = rank * (IBC / 2) + tid; t < (rank + 1) * (IBC / 2); t += PR_T) {
+    const int k = t >> 5, l = t & 31;
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int s = 0; s < PR_S; ++s) {
+      const double* q = part[s / PR_W] + (s % PR_W) * 32 + l;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) acc[d] += q[(d * K + k) * PR_T];
+    }
+    const int64_t il = blk * IBC + t;
+    if (il < a.n_i) finalize_body<float>(a, il, acc[0], acc[1], acc[2]);
+  }
+  cluster.sync();  // the peer's sums stay alive until both CTAs have read them
+  NB_TRACE_END(5);
+  if (a.n_peers) __threadfence_system();
+}
+
 // ---------------------------------------------------------------- split i-block fixup
 template <typename R, int IB>
 __device__ __forceinline__ void fixup_body(const StepArgs<R>& a, int64_t il);
@@ -1438,8 +1702,91 @@ static bool any_split_iblock(const StepArgs<R>& a) {
   return false;
 }
 
+// SMs of the current device (cached per device).
+static int sm_count() {
+  static std::atomic<int> cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c > 0) return c;
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cache[dev].store(sms, std::memory_order_relaxed);
+  return sms;
+}
+
+// Clusters of an FP32 launch through pair_kernel, 0 for the stream-K path: its
+// i-blocks fill one wave of 2-CTA clusters with <= 6 % dead target lanes and
+// every warp's source slice holds at least one full tile.  NB_PAIR=0 / 1 turns
+// it off / on wherever the i-blocks fit one wave (A/B measurements).
+static int pair_clusters(int64_t n_i, int64_t j_count) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("NB_PAIR");
+    env = e ? atoi(e) : -1;
+  }
+  if (env == 0 || n_i < 1) return 0;
+  constexpr int64_t IBC = 32 * NB_PAIR_K;
+  const int64_t waves = sm_count() / PR_CL;
+  const int64_t ncl = (n_i + IBC - 1) / IBC;
+  if (ncl > waves) return 0;
+  if (env != 1 && (n_i * 100 < waves * IBC * 94 || j_count < (int64_t)PR_S * NB_PAIR_TJ)) return 0;
+  return (int)ncl;
+}
+
+template <class Core>
+static const void* pair_fn_of() {
+  return reinterpret_cast<const void*>(&pair_kernel<Core, NB_PAIR_TJ>);
+}
+
+static cudaError_t launch_pair(StepArgs<float> a, int flags, int ncl, cudaStream_t stream) {
+  const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
+  a.uniform_mass = uni ? 1 : 0;
+  const void* fn = mask_self ? (uni ? pair_fn_of<CorePair<true, true>>() : pair_fn_of<CorePair<true, false>>())
+                             : (uni ? pair_fn_of<CorePair<false, true>>() : pair_fn_of<CorePair<false, false>>());
+  const int64_t smem = mask_self ? (uni ? pair_smem_bytes<CorePair<true, true>, NB_PAIR_TJ>()
+                                        : pair_smem_bytes<CorePair<true, false>, NB_PAIR_TJ>())
+                                 : (uni ? pair_smem_bytes<CorePair<false, true>, NB_PAIR_TJ>()
+                                        : pair_smem_bytes<CorePair<false, false>, NB_PAIR_TJ>());
+  {  // opt in to the dynamic shared memory once per (device, kernel)
+    struct Opt { int dev; const void* fn; };
+    static Opt opts[64];
+    static int n_opts = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    bool done = false;
+    for (int k = 0; k < n_opts; ++k) done = done || (opts[k].dev == dev && opts[k].fn == fn);
+    if (!done) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      if (n_opts < 64) opts[n_opts++] = Opt{dev, fn};
+    }
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ncl * PR_CL));
+  cfg.blockDim = dim3(PR_T);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+  count_launch();
+  return e;
+}
+
 template <typename R>
 cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
+  if constexpr (sizeof(R) == 4) {
+    if (const int ncl = pair_clusters(a.n_i, a.j_count)) return launch_pair(a, flags, ncl, stream);
+  }
   const StepGeometry g = step_geometry<R>(a.n_i, a.j_count);
   a.n_tiles = g.n_tiles;
   a.n_iblocks = g.n_iblocks;
@@ -1488,6 +1835,14 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
     count_launch();
   }
   return e;
+}
+
+template <typename R>
+const char* step_kernel_name(int64_t n_i, int64_t j_count) {
+  if constexpr (sizeof(R) == 4) {
+    if (pair_clusters(n_i, j_count)) return "pair_kernel";
+  }
+  return "step_kernel";
 }
 
 template <typename R>
@@ -1629,6 +1984,8 @@ int64_t step_workspace_bytes(int64_t n_i) {
 template StepGeometry step_geometry<float>(int64_t, int64_t);
 template StepGeometry step_geometry<double>(int64_t, int64_t);
 template cudaError_t launch_step<float>(StepArgs<float>, int, cudaStream_t);
+template const char* step_kernel_name<float>(int64_t, int64_t);
+template const char* step_kernel_name<double>(int64_t, int64_t);
 template cudaError_t launch_step<double>(StepArgs<double>, int, cudaStream_t);
 template cudaError_t launch_simulate_persistent<float>(StepArgs<float>, int, V4<float>*, V4<float>*, int64_t,
                                                       cudaStream_t);

@@ -55,6 +55,9 @@ struct StepGeometry {
 template <typename R> StepGeometry step_geometry(int64_t n_i, int64_t j_count);
 // flags: bit 0 exclude the self pair explicitly, bit 1 uniform masses.
 template <typename R> cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t s);
+// Which force kernel launch_step runs for a launch of this shape on the current
+// device: "pair_kernel" (FP32 cluster split-source) or "step_kernel" (stream-K).
+template <typename R> const char* step_kernel_name(int64_t n_i, int64_t j_count);
 template <typename R> int64_t step_workspace_bytes(int64_t n_i);
 // Whole simulate loop (steps drift steps + the final kick) in one cooperative launch.
 template <typename R> cudaError_t launch_simulate_persistent(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b,

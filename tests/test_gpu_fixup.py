@@ -43,7 +43,8 @@ SCRIPT = textwrap.dedent(f"""
 
 
 def _run(path, fixup_kernel):
-    env = dict(os.environ, NB_FIXUP_KERNEL="1" if fixup_kernel else "0")
+    # NB_PAIR=0: the stream-K path (C2-sized FP32 launches would take pair_kernel)
+    env = dict(os.environ, NB_FIXUP_KERNEL="1" if fixup_kernel else "0", NB_PAIR="0")
     r = subprocess.run([sys.executable, "-c", SCRIPT, str(path)], capture_output=True, text=True, timeout=600,
                        env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]

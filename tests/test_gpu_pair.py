@@ -1,0 +1,133 @@
+"""The cluster split-source kernel (pair_kernel: 2-CTA clusters, one i-block of
+224 targets per cluster, 16 warp slices of the sources reduced through
+distributed shared memory; nbody_force.cu) against the long-double oracle.
+
+It is chosen automatically for FP32 launches whose i-blocks fill one wave of
+clusters (C2: N = 16384, and the per-rank size of C3 at 8 GPUs); NB_PAIR=1
+forces it wherever the i-blocks fit one wave, so ragged, tiny, self-masked,
+uniform-mass and carry (sharded) launches are covered here too.  Tolerance:
+the north star's 1e-5 relative per-step acceleration bound
+(_accel_dev, validation.py:212-225)."""
+import os
+import subprocess
+import sys
+import textwrap
+
+import numpy as np
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-5
+
+SCRIPT = textwrap.dedent(f"""
+    import sys, numpy as np
+    sys.path.insert(0, {REPO!r})
+    import paper_2203_08263_b200 as nb
+    from paper_2203_08263_b200.device import DeviceState, kernel_flags
+    from paper_2203_08263_b200._native import NB_MODE_ACCEL
+    out = {{}}
+    cases = [("n1", 1, nb.uniform_cube, 1e-3), ("n33", 33, nb.uniform_cube, 1e-3),
+             ("n4097", 4097, nb.uniform_cube, 1e-3), ("ragged_self", 12345, nb.uniform_cube, 0.0),
+             ("uni", 15000, nb.plummer_sphere, 1e-4), ("c2", 16384, nb.uniform_cube, 1e-2),
+             ("full_wave", 16576, nb.uniform_cube, 1e-3)]
+    for name, n, gen, eps2 in cases:
+        s = gen(n, 3, nb.Precision.SINGLE)
+        pos = s.position_matrix().astype(np.float32)
+        st = DeviceState(pos, np.stack(s.velocities, 1), s.masses, np.float32)
+        f = kernel_flags(s.masses, eps2, np.float32)
+        a = st.accelerations(1.0, eps2, f)[:, :3].cpu().numpy().astype(np.float64)
+        a2 = st.accelerations(1.0, eps2, f)[:, :3].cpu().numpy().astype(np.float64)
+        out[name] = a
+        out[name + "_again"] = a2
+        out[name + "_pos"] = np.concatenate([pos, s.masses[:, None].astype(np.float32)], 1)
+        out[name + "_eps2"] = np.array([eps2])
+    # one rank of a 3-way shard (rows [5000, 10000) of 15000): its own sources
+    # into the FP64 carry, then the circular remainder (run_sharded's two phases)
+    s = nb.uniform_cube(15000, 4, nb.Precision.SINGLE)
+    pos = s.position_matrix().astype(np.float32)
+    st = DeviceState(pos, np.stack(s.velocities, 1), s.masses, np.float32, i_begin=5000, n_i=5000)
+    f = kernel_flags(s.masses, 1e-3, np.float32)
+    st.step(1.0, 1e-3, 0.0, NB_MODE_ACCEL, f, j_begin=5000, j_count=5000, carry_mode=1)
+    st.step(1.0, 1e-3, 0.0, NB_MODE_ACCEL, f, j_begin=10000, j_count=10000, carry_mode=2)
+    out["shard"] = st.acc[:5000, :3].cpu().numpy().astype(np.float64)
+    out["shard_pos"] = np.concatenate([pos, s.masses[:, None].astype(np.float32)], 1)
+    out["shard_eps2"] = np.array([1e-3])
+    # a 3-step trajectory at C2's size through the public API
+    s = nb.uniform_cube(16384, 0, nb.Precision.SINGLE)
+    fin = nb.simulate(s, nb.SimParams(1.0, 1e-2, 1e-2, 3))
+    out["traj"] = fin.position_matrix().astype(np.float64)
+    np.savez(sys.argv[1], **out)
+""")
+
+_cache = {}
+
+
+def _run(tmp_path, pair):
+    if pair in _cache:
+        return _cache[pair]
+    path = tmp_path / f"pair{pair}.npz"
+    env = dict(os.environ, NB_PAIR=str(pair))
+    r = subprocess.run([sys.executable, "-c", SCRIPT, str(path)], capture_output=True, text=True, timeout=900,
+                       env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    _cache[pair] = dict(np.load(path))
+    return _cache[pair]
+
+
+def _rows(n, k=96, seed=5):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, k)]))
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    from oracle import oracle as O
+    return O
+
+
+@pytest.mark.parametrize("name", ["n1", "n33", "n4097", "ragged_self", "uni", "c2", "full_wave"])
+def test_forced_pair_kernel_vs_oracle(name, oracle, tmp_path):
+    d = _run(tmp_path, 1)
+    pos, eps2 = d[name + "_pos"], float(d[name + "_eps2"][0])
+    n = pos.shape[0]
+    rows = _rows(n)
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(4)), rows, 1.0, eps2)
+    got = d[name][rows]
+    assert np.all(np.isfinite(d[name]))
+    if n == 1:  # a lone body feels nothing
+        assert np.all(got == 0.0)
+        return
+    dev = oracle.accel_dev(got, want)
+    print(name, "accel_dev", dev)
+    assert dev <= TOL_F32
+    np.testing.assert_array_equal(d[name], d[name + "_again"])  # bitwise reproducible
+
+
+def test_pair_kernel_sharded_carry_vs_oracle(oracle, tmp_path):
+    d = _run(tmp_path, 1)
+    pos = d["shard_pos"]
+    local = _rows(5000)
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(4)), 5000 + local, 1.0, 1e-3)
+    dev = oracle.accel_dev(d["shard"][local], want)
+    print("shard accel_dev", dev)
+    assert dev <= TOL_F32
+
+
+def test_pair_is_the_default_at_c2_and_stream_k_agrees(oracle, tmp_path):
+    """At C2's size the default path IS the pair kernel (its sums differ in the
+    last bits from stream-K's, NB_PAIR=0), and both match the oracle; the
+    3-step trajectories agree to FP32 rounding."""
+    auto = _run(tmp_path, -1)
+    pair = _run(tmp_path, 1)
+    sk = _run(tmp_path, 0)
+    np.testing.assert_array_equal(auto["c2"], pair["c2"])
+    assert not np.array_equal(sk["c2"], pair["c2"])
+    rows = _rows(16384)
+    pos = sk["c2_pos"]
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(4)), rows, 1.0, 1e-2)
+    assert oracle.accel_dev(sk["c2"][rows], want) <= TOL_F32
+    assert oracle.accel_dev(pair["c2"][rows], want) <= TOL_F32
+    np.testing.assert_array_equal(auto["traj"], pair["traj"])
+    assert oracle.position_dev(pair["traj"], sk["traj"]) <= 1e-5

@@ -51,6 +51,12 @@ VARIANTS = {
     "pg0_infix": {"NB_PARTIAL_GROUPS": 0, "NB_INFIX_DEFAULT": 1},
     "pg1_fixk": {"NB_PARTIAL_GROUPS": 1, "NB_INFIX_DEFAULT": 0},
     "pg1_infix": {"NB_PARTIAL_GROUPS": 1, "NB_INFIX_DEFAULT": 1},
+    # round 2: the cluster split-source kernel with 6 targets per thread (no odd target)
+    "pair_k6": {"NB_PAIR_K": 6},
+    "pair_u8": {"NB_PAIR_UNROLL": 8},
+    "pair_u12": {"NB_PAIR_UNROLL": 12},
+    "pair_u32": {"NB_PAIR_UNROLL": 32},
+    "pair_oddfirst": {"NB_PAIR_ODD_FIRST": 1},
     # extra nvcc flags per variant: {"_flags": ["-Xptxas", "..."]}
 }
 
