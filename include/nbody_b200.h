@@ -113,6 +113,18 @@ int nb_host_simulate_soa_f64(double* px, double* py, double* pz, double* vx, dou
                              double* vz, const double* m, int64_t n, double g, double dt,
                              double eps2, int64_t steps);
 
+/* The same simulate with the inputs left untouched: x, y, z, m, vx, vy, vz
+ * columns in, the final x, y, z, vx, vy, vz into out6 (6*n elements, column
+ * after column), on CUDA device `device` (< 0: the library's current one).
+ * The binding behind simulate()'s single-GPU path (the CPython module
+ * paper_2203_08263_b200._hostpath). */
+int nb_host_simulate_f32(const float* px, const float* py, const float* pz, const float* m,
+                         const float* vx, const float* vy, const float* vz, int64_t n, double g,
+                         double dt, double eps2, int64_t steps, float* out6, int device);
+int nb_host_simulate_f64(const double* px, const double* py, const double* pz, const double* m,
+                         const double* vx, const double* vy, const double* vz, int64_t n, double g,
+                         double dt, double eps2, int64_t steps, double* out6, int device);
+
 /* ---------------------------------------------------------------- device (packed) */
 
 /* Workspace bytes a nb_dev_step_* call needs for an i-shard of n_i bodies;

@@ -95,7 +95,24 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
             raise RuntimeError(f"link failed: {' '.join(link)}\n{r.stdout}\n{r.stderr}")
     with open(stamp, "w") as f:
         f.write(spec + "\n")
+    if lib == LIB:
+        build_hostpath(force)
     return lib
+
+
+def build_hostpath(force: bool = False) -> str:
+    """The CPython binding of simulate()'s single-GPU path (csrc/hostpath.c,
+    gcc against this interpreter's headers), next to the package."""
+    import sysconfig
+    src = os.path.join(CSRC, "hostpath.c")
+    out = os.path.join(PKG, "_hostpath" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if force or _stale(out, [src]):
+        cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
+               src, "-o", out]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"gcc failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return out
 
 
 def build_checked() -> str:

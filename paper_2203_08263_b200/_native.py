@@ -39,6 +39,7 @@ _ARGTYPES = {
     "nb_host_step_soa": [_p] * 9 + [_i64, _d, _i],
     "nb_host_step_aos": [_p] * 5 + [_i64, _d],
     "nb_host_simulate_soa": [_p] * 7 + [_i64, _d, _d, _d, _i64],
+    "nb_host_simulate": [_p] * 7 + [_i64, _d, _d, _d, _i64, _p, _i],
     "nb_dev_step": [_p, _i64, _i64, _i64, _i64, _i64, _d, _d, _d, _i, _i, _p, _i, _p, _p, _p, _p, _i64, _p],
     "nb_dev_step_p2p": [_p, _i64, _i64, _i64, _i64, _i64, _d, _d, _d, _i, _i, _p, _i, _p, _p, _p, _p, _i, _p,
                         _i64, _p],
@@ -104,6 +105,30 @@ def lib() -> ctypes.CDLL:
         _check_digest(L)
         _lib = L
     return _lib
+
+
+_hostpath = None
+
+
+def hostpath():
+    """The CPython binding of nb_host_simulate_f32/f64 (csrc/hostpath.c), bound
+    to this process's loaded library.  ImportError if it was not built: the
+    product path has no fallback."""
+    global _hostpath
+    if _hostpath is None:
+        L = lib()
+        from . import _hostpath as H  # built next to the library by _build.build()
+        H.bind(ctypes.cast(L.nb_host_simulate_f32, ctypes.c_void_p).value,
+               ctypes.cast(L.nb_host_simulate_f64, ctypes.c_void_p).value)
+        _hostpath = H
+    return _hostpath
+
+
+def check(name: str, rc: int) -> None:
+    """Raise NativeError for a nonzero C ABI status returned by ``name``."""
+    if rc != 0:
+        msg = lib().nb_last_error()
+        raise NativeError(name, rc, msg.decode() if msg else "")
 
 
 def call(name: str, *args) -> None:

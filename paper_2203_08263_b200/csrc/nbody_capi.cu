@@ -19,6 +19,18 @@
 #include "nbody_b200.h"
 #include "nbody_kernels.h"
 
+#if NB_TRACE
+#include <chrono>
+// Trace builds: host timestamps (ns, steady clock) of the last simulate_cols
+// call's phases (tools/host_trace.py).
+static double g_ht[16];
+static int g_ht_n = 0;
+#define NB_HT(k) (g_ht[(k)] = (double)std::chrono::duration_cast<std::chrono::nanoseconds>( \
+                      std::chrono::steady_clock::now().time_since_epoch()).count(), g_ht_n = (k) + 1 > g_ht_n ? (k) + 1 : g_ht_n)
+#else
+#define NB_HT(k) ((void)0)
+#endif
+
 namespace nb {
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
@@ -183,11 +195,13 @@ int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, do
     StepArgs<R> a;
     int rc = make_step_args<R>(a, pos_a, n, 0, n, 0, n, g, eps2, dt, NB_STEP_FIRST, flags, nullptr, 0, acc4, vel4,
                                pos_b, ws, ws_bytes, stream, nullptr, 0);
+    NB_HT(8);
     if (rc && rc != -1) return rc;
     if (rc == 0) {
       cudaError_t e = launch_simulate_small<R>(a, flags & (NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS),
                                                static_cast<V4<R>*>(pos_a), static_cast<V4<R>*>(pos_b), steps, st,
                                                cols, cols_out);
+      NB_HT(9);
       if (e == cudaSuccess) {
         if (final_in_b) *final_in_b = (steps & 1) ? 1 : 0;
         if (cols_done) *cols_done = cols ? (cols_out ? 2 : 1) : 0;
@@ -453,11 +467,20 @@ int host_step(R* px, R* py, R* pz, R* vx, R* vy, R* vz, R* pos_aos, R* vel_aos, 
   return download_cols<R>(B, d0, out, counts, 6, n);
 }
 
+// Whole simulate from host columns (inputs x, y, z, m, vx, vy, vz; outputs
+// x, y, z, vx, vy, vz -- may alias the inputs).  One staging memcpy into the
+// arena's pinned block, one H2D; at small N the simulate kernel reads the
+// device column block itself and stores the final columns straight into the
+// pinned block through its device mapping (no pack/unpack launches, no D2H);
+// then one memcpy out.  Stream 0, synchronous.
 template <typename R>
-int host_simulate(R* px, R* py, R* pz, R* vx, R* vy, R* vz, const R* m, int64_t n, double g, double dt,
-                  double eps2, int64_t steps) {
+int host_simulate(const R* px, const R* py, const R* pz, const R* m, const R* vx, const R* vy, const R* vz,
+                  int64_t n, double g, double dt, double eps2, int64_t steps, R* ox, R* oy, R* oz, R* ovx,
+                  R* ovy, R* ovz) {
   if (n < 1) return fail(NB_ERR_ARG, "n must be >= 1");
-  if (!px || !py || !pz || !vx || !vy || !vz || !m) return fail(NB_ERR_ARG, "null host pointer");
+  if (!px || !py || !pz || !vx || !vy || !vz || !m || !ox || !oy || !oz || !ovx || !ovy || !ovz)
+    return fail(NB_ERR_ARG, "null host pointer");
+  NB_HT(0);
   DevBufs B;
   void* pa = B.alloc(sizeof(V4<R>) * n);
   void* pb = B.alloc(sizeof(V4<R>) * n);
@@ -468,23 +491,37 @@ int host_simulate(R* px, R* py, R* pz, R* vx, R* vy, R* vz, const R* m, int64_t 
   void* ws = B.alloc(wsb);  // scratch: no initialisation needed
   if (B.err != cudaSuccess) return cuda_fail(B.err, "cudaMalloc");
   R* d0 = static_cast<R*>(dx);
-  int rc;
-  {
-    const R* cols[7] = {px, py, pz, m, vx, vy, vz};
-    const int counts[7] = {1, 1, 1, 1, 1, 1, 1};
-    if ((rc = upload_cols<R>(B, d0, cols, counts, 7, n))) return rc;
+  R* h = static_cast<R*>(B.pinned(sizeof(R) * 7 * n));
+  if (!h) return cuda_fail(B.err, "cudaMallocHost");
+  NB_HT(1);
+  const R* cols[7] = {px, py, pz, m, vx, vy, vz};
+  for (int c = 0; c < 7; ++c) std::memcpy(h + c * n, cols[c], sizeof(R) * n);
+  NB_HT(2);
+  NB_CUDA(cudaMemcpyAsync(d0, h, sizeof(R) * 7 * n, cudaMemcpyHostToDevice, 0));
+  R* hdev = nullptr;  // the pinned block's device mapping (UVA)
+  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), h, 0) != cudaSuccess) {
+    cudaGetLastError();
+    hdev = nullptr;
   }
-  NB_CUDA(launch_pack_soa<R>(d0, d0 + n, d0 + 2 * n, d0 + 3 * n, static_cast<V4<R>*>(pa), n, 0));
-  NB_CUDA(launch_pack_soa<R>(d0 + 4 * n, d0 + 5 * n, d0 + 6 * n, nullptr, static_cast<V4<R>*>(dv), n, 0));
-  int in_b = 0;
-  if ((rc = dev_simulate<R>(pa, pb, dv, da, n, g, dt, eps2, steps, host_flags<R>(m, n, eps2), ws, wsb,
-                            nullptr, &in_b)))
+  int in_b = 0, done = 0, rc;
+  NB_HT(3);
+  if ((rc = dev_simulate<R>(pa, pb, dv, da, n, g, dt, eps2, steps, host_flags<R>(m, n, eps2), ws, wsb, nullptr,
+                            &in_b, nullptr, d0, &done, hdev)))
     return rc;
-  NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(in_b ? pb : pa), d0, d0 + n, d0 + 2 * n, n, 0));
-  NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(dv), d0 + 3 * n, d0 + 4 * n, d0 + 5 * n, n, 0));
-  R* out[6] = {px, py, pz, vx, vy, vz};
-  const int counts[6] = {1, 1, 1, 1, 1, 1};
-  return download_cols<R>(B, d0, out, counts, 6, n);
+  NB_HT(4);
+  if (!done) {
+    NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(in_b ? pb : pa), d0, d0 + n, d0 + 2 * n, n, 0));
+    NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(dv), d0 + 4 * n, d0 + 5 * n, d0 + 6 * n, n, 0));
+  }
+  if (done != 2) NB_CUDA(cudaMemcpyAsync(h, d0, sizeof(R) * 7 * n, cudaMemcpyDeviceToHost, 0));
+  NB_HT(5);
+  NB_CUDA(cudaStreamSynchronize(0));
+  NB_HT(6);
+  R* outs[7] = {ox, oy, oz, nullptr, ovx, ovy, ovz};
+  for (int c = 0; c < 7; ++c)
+    if (outs[c]) std::memcpy(outs[c], h + c * n, sizeof(R) * n);
+  NB_HT(7);
+  return NB_OK;
 }
 
 template <typename R>
@@ -587,13 +624,16 @@ int dev_simulate_cols(const void* host_cols, void* dev_cols, void* pos_a, void* 
   // One H2D of the column block; the simulate reads it directly (small N) or
   // packs it itself; then the unpack (if the simulate did not write the columns)
   // and one D2H of positions and velocities.
+  NB_HT(0);
   if (n < 1) return fail(NB_ERR_ARG, "need n >= 1");
   if (!host_cols || !dev_cols || !pos_a || !pos_b || !vel4 || !acc4) return fail(NB_ERR_ARG, "null pointer");
   if (!aligned16(pos_a) || !aligned16(vel4)) return fail(NB_ERR_ARG, "pos4/vel4 must be 16-byte aligned");
   if (cudaError_t be = bind_device_of(pos_a)) return cuda_fail(be, "pos4 is not a device pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   R* d = static_cast<R*>(dev_cols);
+  NB_HT(1);
   NB_CUDA(cudaMemcpyAsync(d, host_cols, (size_t)(7 * n) * sizeof(R), cudaMemcpyHostToDevice, st));
+  NB_HT(2);
   if (flags & NB_FLAG_AUTO)  // (while the copy runs) the flags of the staged masses
     flags = (flags & ~(NB_FLAG_AUTO | NB_FLAG_EXCLUDE_SELF | NB_FLAG_UNIFORM_MASS)) |
             host_flags<R>(static_cast<const R*>(host_cols) + 3 * n, n, eps2);
@@ -606,8 +646,10 @@ int dev_simulate_cols(const void* host_cols, void* dev_cols, void* pos_a, void* 
     hdev = nullptr;
   }
   int in_b = 0, done = 0;
+  NB_HT(3);
   int rc = dev_simulate<R>(pos_a, pos_b, vel4, acc4, n, g, dt, eps2, steps, flags, ws, ws_bytes, stream, &in_b,
                            nullptr, d, &done, hdev);
+  NB_HT(4);
   if (rc) return rc;
   if (final_in_b) *final_in_b = in_b;
   if (!done) {
@@ -619,7 +661,9 @@ int dev_simulate_cols(const void* host_cols, void* dev_cols, void* pos_a, void* 
   if (done != 2)
     NB_CUDA(cudaMemcpyAsync(const_cast<void*>(host_cols), d, (size_t)(7 * n) * sizeof(R), cudaMemcpyDeviceToHost,
                             st));
+  NB_HT(5);
   NB_CUDA(cudaStreamSynchronize(st));
+  NB_HT(6);
   return NB_OK;
 }
 
@@ -705,11 +749,33 @@ int nb_host_step_aos_f64(double* pos, double* vel, const double* ax, const doubl
 }
 int nb_host_simulate_soa_f32(float* px, float* py, float* pz, float* vx, float* vy, float* vz, const float* m,
                              int64_t n, double g, double dt, double eps2, int64_t steps) {
-  return host_simulate<float>(px, py, pz, vx, vy, vz, m, n, g, dt, eps2, steps);
+  return host_simulate<float>(px, py, pz, m, vx, vy, vz, n, g, dt, eps2, steps, px, py, pz, vx, vy, vz);
 }
 int nb_host_simulate_soa_f64(double* px, double* py, double* pz, double* vx, double* vy, double* vz,
                              const double* m, int64_t n, double g, double dt, double eps2, int64_t steps) {
-  return host_simulate<double>(px, py, pz, vx, vy, vz, m, n, g, dt, eps2, steps);
+  return host_simulate<double>(px, py, pz, m, vx, vy, vz, n, g, dt, eps2, steps, px, py, pz, vx, vy, vz);
+}
+int nb_host_simulate_f32(const float* px, const float* py, const float* pz, const float* m, const float* vx,
+                         const float* vy, const float* vz, int64_t n, double g, double dt, double eps2,
+                         int64_t steps, float* out6, int device) {
+  if (!out6) return fail(NB_ERR_ARG, "null host pointer");
+  if (device >= 0) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != device) NB_CUDA(cudaSetDevice(device));
+  }
+  return host_simulate<float>(px, py, pz, m, vx, vy, vz, n, g, dt, eps2, steps, out6, out6 + n, out6 + 2 * n,
+                              out6 + 3 * n, out6 + 4 * n, out6 + 5 * n);
+}
+int nb_host_simulate_f64(const double* px, const double* py, const double* pz, const double* m, const double* vx,
+                         const double* vy, const double* vz, int64_t n, double g, double dt, double eps2,
+                         int64_t steps, double* out6, int device) {
+  if (!out6) return fail(NB_ERR_ARG, "null host pointer");
+  if (device >= 0) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != device) NB_CUDA(cudaSetDevice(device));
+  }
+  return host_simulate<double>(px, py, pz, m, vx, vy, vz, n, g, dt, eps2, steps, out6, out6 + n, out6 + 2 * n,
+                               out6 + 3 * n, out6 + 4 * n, out6 + 5 * n);
 }
 
 int64_t nb_dev_workspace_bytes(int precision_bytes, int64_t n_i) {
@@ -894,6 +960,11 @@ __attribute__((visibility("default"))) int nb_trace_setup(void* buf, int64_t cap
   return nb::trace_setup(buf, capacity);
 }
 __attribute__((visibility("default"))) int64_t nb_trace_count(void) { return nb::trace_count(); }
+__attribute__((visibility("default"))) int nb_host_trace(double* out, int cap) {
+  const int k = g_ht_n < cap ? g_ht_n : cap;
+  for (int q = 0; q < k; ++q) out[q] = g_ht[q];
+  return k;
+}
 #endif
 // ---------------------------------------------------------------- position exchange (NCCL)
 // The per-step exchange of SURVEY.md 8(e) behind the C ABI, for hosts that are

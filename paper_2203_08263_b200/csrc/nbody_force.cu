@@ -1424,6 +1424,10 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
     a.pos_next = (st & 1) ? pos_a : pos_b;
     // step 0 of a column-block run: the packed buffer holds no state yet
     a.mass0 = (cols && st == 0) ? cols + 3 * n : nullptr;
+#if NB_TRACE
+    unsigned long long tt[5];
+    tt[0] = gtimer();
+#endif
     for (int64_t j = tid; j < n; j += SN_T) {  // positions moved last step: coherent loads
       B b;
       if (cols && st == 0) {
@@ -1438,6 +1442,9 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
       if (Core::NEEDS_LM) slm[slot(j)] = lg2_mufu((float)b.w);
     }
     __syncthreads();
+#if NB_TRACE
+    tt[1] = gtimer();
+#endif
     const int64_t ia = i0 < n ? i0 : n - 1, ib = i0 + 1 < n ? i0 + 1 : n - 1;
     core.set_pair(0, sp[slot(ia)], sp[slot(ib)]);
     core.zero_sums();
@@ -1455,6 +1462,9 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
 #pragma unroll 1
     for (; jj < cnt; ++jj) core.interact(tb[jj], jj);
     core.end_tile();
+#if NB_TRACE
+    tt[2] = gtimer();
+#endif
     // S splits -> 1: butterfly over the lane groups (a + b == b + a, so every
     // lane ends with the same bits), then the 8 warps in ascending order.
     double v[6];
@@ -1494,7 +1504,15 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
         co[6 * n + il] = vel.z;
       }
     }
+#if NB_TRACE
+    __syncthreads();
+    tt[3] = gtimer();
+#endif
     if (st < steps) grid.sync();  // new positions visible; nobody still reads the old buffer, sp or red
+#if NB_TRACE
+    tt[4] = gtimer();
+    trace_put(6, (unsigned long long)blockIdx.x | ((unsigned long long)st << 32), tt, 5);
+#endif
   }
 }
 

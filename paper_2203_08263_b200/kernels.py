@@ -128,8 +128,13 @@ class AccelerationBuffer:
 
 # --------------------------------------------------------------------------- boundary helpers
 
+_PRECISION_DTYPE = {"single": np.dtype(np.float32), "double": np.dtype(np.float64)}
+
+
 def _dtype(sys_) -> np.dtype:
-    return Precision(_value(sys_.precision)).dtype
+    p = _value(sys_.precision)
+    dt = _PRECISION_DTYPE.get(p) if isinstance(p, str) else None
+    return dt if dt is not None else Precision(p).dtype
 
 
 def _count(sys_) -> int:
@@ -172,11 +177,11 @@ def _check_buffers(sys_) -> None:
     this raises the same before any device work instead of casting."""
     want = _dtype(sys_)
     if _value(sys_.layout) == "soa":
-        arrays = [*sys_.positions, *sys_.velocities, sys_.masses]
+        arrays = (*sys_.positions, *sys_.velocities, sys_.masses)
     else:
-        arrays = [sys_.positions, sys_.velocities, sys_.masses]
+        arrays = (sys_.positions, sys_.velocities, sys_.masses)
     for a in arrays:
-        got = np.asarray(a).dtype
+        got = a.dtype if isinstance(a, np.ndarray) else np.asarray(a).dtype
         if got != want:
             raise ValueError(f"Buffer dtype mismatch, expected '{_CTYPE.get(want, want)}' but got "
                              f"'{_CTYPE.get(got, got)}' (system precision is {_value(sys_.precision)})")
@@ -328,18 +333,27 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
         _store(state, "positions", pos)
         _store(state, "velocities", vel)
         return state
-    # Single GPU: columns go straight into the pinned column staging of the
-    # resident state (one H2D; at small N the simulate kernel reads and writes
-    # the columns itself) and the result columns come back in one D2H; the
-    # kernel flags are derived from the staged masses inside the native call.
-    from ._native import NB_FLAG_AUTO
-    m = np.asarray(sys_.masses, dtype)
-    with _STATE_LOCK:
-        pc, vc = _columns(sys_, "positions"), _columns(sys_, "velocities")
-        st = _resident_state(pc, vc, m, dtype, load=False)
-        # upload, simulate and read back in one native call (nb_dev_simulate_cols)
-        pos, vel = st.simulate_columns(pc, vc, m, params.gravitational_constant, params.dt, params.softening_sq,
-                                       params.steps, NB_FLAG_AUTO)
+    # Single GPU: ONE native call through the CPython binding (_hostpath, the
+    # buffer protocol -- no per-array ctypes pointer extraction) into
+    # nb_host_simulate: the columns are staged into the library's pinned block,
+    # uploaded once, simulated (at small N the simulate kernel reads the device
+    # columns and stores the final state straight into the pinned block) and
+    # copied into one fresh 6*N result block; the kernel flags come from the
+    # masses inside the call.
+    import torch
+
+    from . import _native
+    pc, vc = _columns(sys_, "positions"), _columns(sys_, "velocities")
+    if _value(sys_.layout) != "soa":  # (N, 3) blocks: contiguous column copies
+        pc = tuple(np.ascontiguousarray(c) for c in pc)
+        vc = tuple(np.ascontiguousarray(c) for c in vc)
+    out = np.empty(6 * n, dtype)
+    rc = _native.hostpath().simulate(pc[0], pc[1], pc[2], sys_.masses, vc[0], vc[1], vc[2], out,
+                                     params.gravitational_constant, params.dt, params.softening_sq,
+                                     params.steps, torch.cuda.current_device())
+    _native.check("nb_host_simulate", rc)
+    pos = (out[:n], out[n:2 * n], out[2 * n:3 * n])
+    vel = (out[3 * n:4 * n], out[4 * n:5 * n], out[5 * n:])
     if _value(sys_.layout) != "soa":
         pos, vel = np.stack(pos, 1), np.stack(vel, 1)
     return type(sys_)(sys_.layout, sys_.precision, pos, vel, sys_.masses.copy())

@@ -47,6 +47,22 @@ sim()
 torch.cuda.synchronize()
 n = L.nb_trace_count()
 r = buf[: 8 * min(n, cap)].view(-1, 8).cpu().numpy()
+if (r[:, 0] == 6).any():  # small-N kernel: per CTA per step (start, staged, computed, reduced+stored, synced)
+    p = r[r[:, 0] == 6]
+    step = p[:, 1] >> 32
+    print(f"# {name}: small-N kernel, {len(p)} (CTA, step) records; per step, us (median over CTAs; "
+          "compute = thread 0's source loop)\n")
+    print("| step | stage | compute | reduce + epilogue | grid sync | step total |")
+    print("|---|---|---|---|---|---|")
+    for k in np.unique(step):
+        q = p[step == k]
+        t0, t1, t2, t3, t4 = (q[:, 3 + i].astype(np.float64) for i in range(5))
+        tot = (np.median(t4 - t0)) / 1e3
+        print(f"| {k} | {np.median(t1 - t0) / 1e3:.2f} | {np.median(t2 - t1) / 1e3:.2f} | "
+              f"{np.median(t3 - t2) / 1e3:.2f} | {np.median(t4 - t3) / 1e3:.2f} | {tot:.2f} |")
+    starts = [p[step == k][:, 3].min() for k in np.unique(step)]
+    print(f"\nstep period (first CTA start to next): {np.median(np.diff(starts)) / 1e3:.2f} us")
+    sys.exit(0)
 if (r[:, 0] == 3).any():  # persistent simulate_kernel: per CTA per step (start, pass, sync1, fixup, sync2)
     p = r[r[:, 0] == 3]
     step = p[:, 1] >> 32
