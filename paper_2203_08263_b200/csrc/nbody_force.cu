@@ -1345,7 +1345,10 @@ __global__ void __launch_bounds__(T, MINB) simulate_kernel(StepArgs<typename Cor
 // banks), then one grid barrier per step (per-CTA release/acquire flags in its
 // place measured slower beyond ~32 CTAs: every CTA polls every flag).  Same Core arithmetic as the main kernel (the FP32 split is
 // <= N/S terms in FP32 before the FP64 sums).
-constexpr int SN_T = 256;  // threads per CTA (8 warps)
+#ifndef NB_SMALL_T
+#define NB_SMALL_T 256
+#endif
+constexpr int SN_T = NB_SMALL_T;  // threads per CTA (8 warps)
 
 // Bodies per split in shared memory: ceil(N/S) rounded up to 1 mod 8, so the
 // splits of one warp's lane groups start 4 banks apart (FP32 bodies; FP64 ones
