@@ -529,16 +529,26 @@ def run_ours(args) -> dict:
     e2e = None
     if not args.no_e2e:
         sys_host = cfg.system()
+        tw = time.perf_counter()
         for _ in range(args.warmup):
             nb.simulate(sys_host, params)
         torch.cuda.synchronize()
+        # Sub-millisecond simulates (C1: ~75 us) are timed over at least ~50 ms
+        # of calls so the rate is not a handful of calls' jitter; every call is
+        # a full simulate with its own uploads and readback.
+        per_call = (time.perf_counter() - tw) / max(1, args.warmup)
+        calls = max(args.steps, min(2000, int(0.05 / max(per_call, 1e-6)) + 1))
+        if world > 1:  # every rank runs the same number of calls
+            t = torch.tensor([calls], dtype=torch.int64, device=dev if backend == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            calls = int(t.item())
         barrier()
         t0 = time.perf_counter()
         final = None
-        for _ in range(args.steps):
+        for _ in range(calls):
             final = nb.simulate(sys_host, params)
         torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
+        e2e_s = (time.perf_counter() - t0) * args.steps / calls
         if world > 1:
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -558,7 +568,8 @@ def run_ours(args) -> dict:
                "d2h_bytes_per_step": d2h,
                "api": "paper_2203_08263_b200.simulate(ParticleSystem, SimParams) from host NumPy arrays"
                       + (f" on each of {world} ranks (i-sharded; bytes summed over ranks)" if world > 1 else ""),
-               "checksum": nb.checksum(final)}
+               "checksum": nb.checksum(final),
+               "calls_timed": calls}
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -20,15 +20,12 @@
 #include "nbody_kernels.h"
 
 #if NB_TRACE
-#include <chrono>
-// Trace builds: host timestamps (ns, steady clock) of the last simulate_cols
-// call's phases (tools/host_trace.py).
-static double g_ht[16];
-static int g_ht_n = 0;
-#define NB_HT(k) (g_ht[(k)] = (double)std::chrono::duration_cast<std::chrono::nanoseconds>( \
-                      std::chrono::steady_clock::now().time_since_epoch()).count(), g_ht_n = (k) + 1 > g_ht_n ? (k) + 1 : g_ht_n)
-#else
-#define NB_HT(k) ((void)0)
+namespace nb {
+double g_ht[16];
+int g_ht_n = 0;
+}  // namespace nb
+using nb::g_ht;
+using nb::g_ht_n;
 #endif
 
 namespace nb {
@@ -96,6 +93,11 @@ cudaError_t bind_device_of(const void* p) {
 }
 
 template <typename R>
+void fill_step_args(StepArgs<R>& a, const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
+                    int64_t j_count, double g, double eps2, double dt, int mode, double* carry, int carry_mode,
+                    void* acc4, void* vel4, void* pos4_next, void* workspace, void* const* peers, int n_peers);
+
+template <typename R>
 int make_step_args(StepArgs<R>& a, const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
              int64_t j_count, double g, double eps2, double dt, int mode, int flags,
              double* carry, int carry_mode, void* acc4, void* vel4, void* pos4_next,
@@ -129,7 +131,17 @@ int make_step_args(StepArgs<R>& a, const void* pos4, int64_t n_all, int64_t i_be
   const int64_t need = step_workspace_bytes<R>(n_i);
   if (!workspace || workspace_bytes < need)
     return fail(NB_ERR_WORKSPACE, "workspace smaller than nb_dev_workspace_bytes(): need " + std::to_string(need));
+  fill_step_args<R>(a, pos4, n_all, i_begin, n_i, j_begin, j_count, g, eps2, dt, mode, carry, carry_mode, acc4, vel4,
+                    pos4_next, workspace, peers, n_peers);
+  return NB_OK;
+}
 
+// The StepArgs of a launch, unchecked: make_step_args validates first; the
+// host entry points that allocated every buffer themselves call it directly.
+template <typename R>
+void fill_step_args(StepArgs<R>& a, const void* pos4, int64_t n_all, int64_t i_begin, int64_t n_i, int64_t j_begin,
+                    int64_t j_count, double g, double eps2, double dt, int mode, double* carry, int carry_mode,
+                    void* acc4, void* vel4, void* pos4_next, void* workspace, void* const* peers, int n_peers) {
   a = StepArgs<R>{};
   a.pos = static_cast<const V4<R>*>(pos4);
   a.n_all = n_all; a.i_begin = i_begin; a.n_i = n_i; a.j_begin = j_begin; a.j_count = j_count;
@@ -144,8 +156,6 @@ int make_step_args(StepArgs<R>& a, const void* pos4, int64_t n_all, int64_t i_be
   a.slots = reinterpret_cast<double*>(static_cast<char*>(workspace) + workspace_header_bytes<R>());
   a.n_peers = n_peers;
   for (int q = 0; q < n_peers; ++q) a.peers[q] = static_cast<V4<R>*>(peers[q]);
-  (void)stream;
-  return NB_OK;
 }
 
 template <typename R>
@@ -304,6 +314,9 @@ struct Arena {
   size_t cap[12] = {};
   void* host = nullptr;  // pinned staging: each call's uploads (and then downloads) as one block
   size_t host_cap = 0;
+  // nb_host_simulate's own non-blocking stream: a launch on the legacy stream 0
+  // costs ~1.6 us more host time (tools/api_cost.cu), which is on C1's path.
+  cudaStream_t stream = nullptr;
 };
 std::mutex g_arena_mu;
 Arena g_arenas[32];
@@ -334,6 +347,10 @@ struct DevBufs {
       A->cap[k] = bytes;
     }
     return A->p[k];
+  }
+  cudaStream_t stream() {
+    if (err == cudaSuccess && !A->stream) err = cudaStreamCreateWithFlags(&A->stream, cudaStreamNonBlocking);
+    return A->stream;
   }
   void* pinned(size_t bytes) {
     if (err != cudaSuccess) return nullptr;
@@ -493,29 +510,54 @@ int host_simulate(const R* px, const R* py, const R* pz, const R* m, const R* vx
   R* d0 = static_cast<R*>(dx);
   R* h = static_cast<R*>(B.pinned(sizeof(R) * 7 * n));
   if (!h) return cuda_fail(B.err, "cudaMallocHost");
+  cudaStream_t st = B.stream();
+  if (!st) return cuda_fail(B.err, "cudaStreamCreate");
   NB_HT(1);
   const R* cols[7] = {px, py, pz, m, vx, vy, vz};
   for (int c = 0; c < 7; ++c) std::memcpy(h + c * n, cols[c], sizeof(R) * n);
   NB_HT(2);
-  NB_CUDA(cudaMemcpyAsync(d0, h, sizeof(R) * 7 * n, cudaMemcpyHostToDevice, 0));
   R* hdev = nullptr;  // the pinned block's device mapping (UVA)
   if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&hdev), h, 0) != cudaSuccess) {
     cudaGetLastError();
     hdev = nullptr;
   }
+  const bool small = steps >= 1 && dt > 0.0 && g == g && eps2 >= 0.0 && n <= small_max_n((int)sizeof(R));
+  // (An H2D copy: reading the columns through the mapping inside the kernel
+  // measured no faster at C1 -- the copy overlaps the launch's host time.)
+  NB_CUDA(cudaMemcpyAsync(d0, h, sizeof(R) * 7 * n, cudaMemcpyHostToDevice, st));
   int in_b = 0, done = 0, rc;
+  const int flags = host_flags<R>(m, n, eps2);
   NB_HT(3);
-  if ((rc = dev_simulate<R>(pa, pb, dv, da, n, g, dt, eps2, steps, host_flags<R>(m, n, eps2), ws, wsb, nullptr,
-                            &in_b, nullptr, d0, &done, hdev)))
+  bool launched = false;
+  if (small) {
+    // every buffer is this call's own: the small-N launch without re-validation
+    StepArgs<R> a;
+    fill_step_args<R>(a, pa, n, 0, n, 0, n, g, eps2, dt, NB_STEP_FIRST, nullptr, 0, da, dv, pb, ws, nullptr, 0);
+    NB_HT(8);
+    const cudaError_t e = launch_simulate_small<R>(a, flags, static_cast<V4<R>*>(pa), static_cast<V4<R>*>(pb), steps,
+                                                   st, d0, hdev);
+    NB_HT(9);
+    if (e == cudaSuccess) {
+      launched = true;
+      in_b = (steps & 1) ? 1 : 0;
+      done = hdev ? 2 : 1;
+    } else if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported) {
+      return cuda_fail(e, "small_simulate_kernel");
+    } else {
+      cudaGetLastError();
+    }
+  }
+  if (!launched && (rc = dev_simulate<R>(pa, pb, dv, da, n, g, dt, eps2, steps, flags, ws, wsb, st, &in_b,
+                                         nullptr, d0, &done, hdev)))
     return rc;
   NB_HT(4);
   if (!done) {
-    NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(in_b ? pb : pa), d0, d0 + n, d0 + 2 * n, n, 0));
-    NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(dv), d0 + 4 * n, d0 + 5 * n, d0 + 6 * n, n, 0));
+    NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(in_b ? pb : pa), d0, d0 + n, d0 + 2 * n, n, st));
+    NB_CUDA(launch_unpack_soa<R>(static_cast<V4<R>*>(dv), d0 + 4 * n, d0 + 5 * n, d0 + 6 * n, n, st));
   }
-  if (done != 2) NB_CUDA(cudaMemcpyAsync(h, d0, sizeof(R) * 7 * n, cudaMemcpyDeviceToHost, 0));
+  if (done != 2) NB_CUDA(cudaMemcpyAsync(h, d0, sizeof(R) * 7 * n, cudaMemcpyDeviceToHost, st));
   NB_HT(5);
-  NB_CUDA(cudaStreamSynchronize(0));
+  NB_CUDA(cudaStreamSynchronize(st));
   NB_HT(6);
   R* outs[7] = {ox, oy, oz, nullptr, ovx, ovy, ovz};
   for (int c = 0; c < 7; ++c)

@@ -1924,8 +1924,9 @@ cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>*
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
   const int64_t n = a.n_all;
+  NB_HT(10);
   int ppw = n <= (sizeof(R) == 4 ? 3072 : 1184) ? 4 : 8;
-  if (const char* env = getenv("NB_SMALL_PPW")) ppw = atoi(env) == 4 ? 4 : 8;
+  if (const char* env = getenv("NB_SMALL_PPW")) ppw = atoi(env) == 4 ? 4 : 8;  // (read per call: tools/small_n_bench.py)
   const void* fn = ppw == 4 ? small_fn<R, 4>(mask_self, uni) : small_fn<R, 8>(mask_self, uni);
   bool needs_lm = false;
   if constexpr (sizeof(R) == 4) needs_lm = !uni && SmallF32<false, false>::NEEDS_LM;
@@ -1965,11 +1966,14 @@ cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>*
     if (n_caps < 64) caps[n_caps++] = Cap{dev, fn, smem, capacity};
   }
   lock.unlock();
+  NB_HT(11);
   const int64_t grid = (n + 2 * ppw - 1) / (2 * ppw);
   if (grid > (int64_t)capacity) return cudaErrorCooperativeLaunchTooLarge;
   int64_t L = small_split_stride(n, (SN_T / 32) * (32 / ppw));
   void* args[] = {&a, &pos_a, &pos_b, &steps, &L, &cols, &cols_out};
+  NB_HT(12);
   cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(SN_T), args, (size_t)smem, stream);
+  NB_HT(13);
   count_launch();
   return e;
 }

@@ -6,6 +6,21 @@
 
 #include "nbody_common.cuh"
 
+#if NB_TRACE
+#include <chrono>
+namespace nb {
+// Trace builds: host timestamps (ns, steady clock) of the last host simulate
+// call's phases (tools/host_trace.py); defined in nbody_capi.cu.
+extern double g_ht[16];
+extern int g_ht_n;
+}  // namespace nb
+#define NB_HT(k) (nb::g_ht[(k)] = (double)std::chrono::duration_cast<std::chrono::nanoseconds>( \
+                      std::chrono::steady_clock::now().time_since_epoch()).count(), \
+                  nb::g_ht_n = (k) + 1 > nb::g_ht_n ? (k) + 1 : nb::g_ht_n)
+#else
+#define NB_HT(k) ((void)0)
+#endif
+
 namespace nb {
 
 enum : int {

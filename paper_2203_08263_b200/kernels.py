@@ -202,9 +202,9 @@ def _check(sys_, variant, out) -> None:
 
 
 def _distributed_world(group) -> int:
-    try:
-        import torch.distributed as dist
-    except ImportError:  # pragma: no cover
+    import sys
+    dist = sys.modules.get("torch.distributed")
+    if dist is None:  # never imported: no process group can exist
         return 1
     if not dist.is_available() or not dist.is_initialized():
         return 1
@@ -340,23 +340,40 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
     # columns and stores the final state straight into the pinned block) and
     # copied into one fresh 6*N result block; the kernel flags come from the
     # masses inside the call.
-    import torch
+    hp, device = _host_binding()
+    soa = _value(sys_.layout) == "soa"
+    if soa:
+        (px, py, pz), (vx, vy, vz) = sys_.positions, sys_.velocities
+    else:  # (N, 3) blocks: contiguous column copies
+        px, py, pz, vx, vy, vz = (np.ascontiguousarray(c) for c in
+                                  (*_columns(sys_, "positions"), *_columns(sys_, "velocities")))
+    out = np.empty((6, n), dtype)
+    rc = hp.simulate(px, py, pz, sys_.masses, vx, vy, vz, out, params.gravitational_constant, params.dt,
+                     params.softening_sq, params.steps, device())
+    if rc:
+        from . import _native
+        _native.check("nb_host_simulate", rc)
+    x, y, z, ux, uy, uz = out
+    if soa:
+        return type(sys_)(sys_.layout, sys_.precision, (x, y, z), (ux, uy, uz), sys_.masses.copy())
+    return type(sys_)(sys_.layout, sys_.precision, np.stack((x, y, z), 1), np.stack((ux, uy, uz), 1),
+                      sys_.masses.copy())
 
-    from . import _native
-    pc, vc = _columns(sys_, "positions"), _columns(sys_, "velocities")
-    if _value(sys_.layout) != "soa":  # (N, 3) blocks: contiguous column copies
-        pc = tuple(np.ascontiguousarray(c) for c in pc)
-        vc = tuple(np.ascontiguousarray(c) for c in vc)
-    out = np.empty(6 * n, dtype)
-    rc = _native.hostpath().simulate(pc[0], pc[1], pc[2], sys_.masses, vc[0], vc[1], vc[2], out,
-                                     params.gravitational_constant, params.dt, params.softening_sq,
-                                     params.steps, torch.cuda.current_device())
-    _native.check("nb_host_simulate", rc)
-    pos = (out[:n], out[n:2 * n], out[2 * n:3 * n])
-    vel = (out[3 * n:4 * n], out[4 * n:5 * n], out[5 * n:])
-    if _value(sys_.layout) != "soa":
-        pos, vel = np.stack(pos, 1), np.stack(vel, 1)
-    return type(sys_)(sys_.layout, sys_.precision, pos, vel, sys_.masses.copy())
+
+_HOST = None
+
+
+def _host_binding():
+    """(the bound _hostpath module, the current-CUDA-device function), resolved
+    once: simulate()'s per-call host cost is on C1's critical path."""
+    global _HOST
+    if _HOST is None:
+        import torch
+
+        from . import _native
+        torch.cuda.init()
+        _HOST = (_native.hostpath(), torch._C._cuda_getDevice)
+    return _HOST
 
 
 def diagnostics_gpu(sys_, params) -> dict:

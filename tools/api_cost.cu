@@ -15,6 +15,14 @@ __global__ void coop_kernel(int* p, int steps) {
   if (p && threadIdx.x == 1 << 30) *p = 0;
 }
 
+struct BigArg { char b[296]; };
+__global__ void coop_big(BigArg a, int steps) {
+  extern __shared__ char sm[];
+  cooperative_groups::grid_group g = cooperative_groups::this_grid();
+  for (int s = 0; s < steps; ++s) g.sync();
+  if (threadIdx.x == 1 << 30) sm[0] = a.b[0];
+}
+
 template <class F>
 static double us(F f, int reps = 2000) {
   f();
@@ -79,5 +87,37 @@ int main() {
     cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st);
     cudaLaunchCooperativeKernel((void*)coop_kernel, 128, 256, args, 0, st);
     cudaStreamSynchronize(st); }));
+  // r02: simulate()'s launch in context -- legacy stream 0 vs a non-blocking
+  // stream, 40 KB of dynamic shared memory, a 300-byte parameter block, and a
+  // CUDA graph of (H2D + cooperative kernel) replayed
+  BigArg big = {};
+  int ss = 0;
+  void* args2[] = {&big, &ss};
+  cudaFuncSetAttribute((void*)coop_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+  for (int pass = 0; pass < 2; ++pass) {
+    cudaStream_t s2 = pass ? st : (cudaStream_t)0;
+    const char* nm = pass ? "non-blocking stream" : "legacy stream 0";
+    cudaDeviceSynchronize();
+    std::printf("coop 128x256, 40KB dyn smem, 300B params, %-20s %8.2f us\n", nm,
+                us([&] { cudaLaunchCooperativeKernel((void*)coop_big, 128, 256, args2, 40 * 1024, s2); }, 200));
+    cudaDeviceSynchronize();
+    std::printf("H2D + that coop + sync, %-35s %8.2f us\n", nm, us([&] {
+      cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s2);
+      cudaLaunchCooperativeKernel((void*)coop_big, 128, 256, args2, 40 * 1024, s2);
+      cudaStreamSynchronize(s2); }, 500));
+  }
+  cudaGraph_t gr;
+  cudaGraphExec_t ge;
+  cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st);
+  cudaError_t ce = cudaLaunchCooperativeKernel((void*)coop_big, 128, 256, args2, 40 * 1024, st);
+  cudaError_t ee = cudaStreamEndCapture(st, &gr);
+  cudaError_t ie = cudaGraphInstantiate(&ge, gr, 0);
+  std::printf("graph capture: launch %d, end %d, instantiate %d\n", (int)ce, (int)ee, (int)ie);
+  if (ie == cudaSuccess) {
+    std::printf("%-58s %8.2f us\n", "graph launch (H2D + coop) async", us([&] { cudaGraphLaunch(ge, st); }, 200));
+    cudaDeviceSynchronize();
+    std::printf("%-58s %8.2f us\n", "graph launch (H2D + coop) + sync", us([&] { cudaGraphLaunch(ge, st); cudaStreamSynchronize(st); }, 500));
+  }
   return 0;
 }

@@ -18,7 +18,7 @@ buf = (ctypes.c_double * 16)()
 names = ["arena + checks", "staging memcpy", "H2D + map", "launch (dev_simulate)", "D2H enqueue", "stream sync", "memcpy out"]
 acc = {k: [] for k in names}
 tot, outer = [], []
-sub = ([], [])
+sub = ([], [], [], [], [])
 for r in range(reps + 20):
     t0 = time.perf_counter_ns()
     nb.simulate(s, p)
@@ -32,6 +32,10 @@ for r in range(reps + 20):
         if k >= 10:
             sub[0].append((t[8] - t[3]) / 1e3)
             sub[1].append((t[9] - t[8]) / 1e3)
+        if k >= 14:
+            sub[2].append((t[11] - t[10]) / 1e3)
+            sub[3].append((t[12] - t[11]) / 1e3)
+            sub[4].append((t[13] - t[12]) / 1e3)
         outer.append((t1 - t0) / 1e3)
 print(f"# {name}: nb.simulate host phases, median of {reps} calls (us)")
 for nm in names:
@@ -39,5 +43,8 @@ for nm in names:
 print(f"{'native call total':28s} {np.median(tot):8.2f}")
 print(f"{'  of launch: make_step_args':28s} {np.median(sub[0]):8.2f}")
 print(f"{'  of launch: small launch':28s} {np.median(sub[1]):8.2f}")
+print(f"{'    prep (caches, ppw)':28s} {np.median(sub[2]):8.2f}")
+print(f"{'    args':28s} {np.median(sub[3]):8.2f}")
+print(f"{'    cudaLaunchCooperativeKernel':28s} {np.median(sub[4]):8.2f}")
 print(f"{'nb.simulate end to end':28s} {np.median(outer):8.2f}")
 print(f"{'python outside the call':28s} {np.median(np.array(outer) - np.array(tot)):8.2f}")
