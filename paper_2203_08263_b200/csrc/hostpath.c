@@ -10,12 +10,14 @@
  * NB_LIB_PATH variants included) with the GIL released.
  *
  *   bind(addr_f32, addr_f64)
- *   simulate(px, py, pz, m, vx, vy, vz, out6, g, dt, eps2, steps, device) -> rc
+ *   simulate(px, py, pz, m, vx, vy, vz, out6, g, dt, eps2, steps, device, itemsize) -> rc
  *
- * Every array must be C-contiguous with the same float32/float64 item type;
- * inputs hold n elements, out6 holds 6*n.  Returns the C ABI's status (the
- * caller raises with nb_last_error on nonzero); TypeError/ValueError for bad
- * buffers, RuntimeError when unbound. */
+ * Every array must be C-contiguous with the float32 (itemsize 4) or float64
+ * (8) item type the system precision names; inputs hold n elements, out6
+ * holds 6*n.  Returns the C ABI's status (the caller raises with nb_last_error
+ * on nonzero); TypeError for a buffer of another item type (the caller then
+ * raises the reference's dtype ValueError), ValueError for bad lengths,
+ * RuntimeError when unbound. */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
 #include <stdint.h>
@@ -50,29 +52,28 @@ static PyObject* simulate(PyObject* self, PyObject* args) {
   PyObject* objs[8];
   double g, dt, eps2;
   long long steps;
-  int device;
+  int device, want;
   (void)self;
-  if (!PyArg_ParseTuple(args, "OOOOOOOOdddLi", &objs[0], &objs[1], &objs[2], &objs[3], &objs[4], &objs[5],
-                        &objs[6], &objs[7], &g, &dt, &eps2, &steps, &device))
+  if (!PyArg_ParseTuple(args, "OOOOOOOOdddLii", &objs[0], &objs[1], &objs[2], &objs[3], &objs[4], &objs[5],
+                        &objs[6], &objs[7], &g, &dt, &eps2, &steps, &device, &want))
     return NULL;
   if (!g_f32 || !g_f64) {
     PyErr_SetString(PyExc_RuntimeError, "_hostpath is not bound to libnbody_b200.so (call bind first)");
     return NULL;
   }
   Py_buffer v[8];
-  int got = 0, kind = 0, rc = 0;
+  int got = 0, kind = want, rc = 0;
   Py_ssize_t n = -1;
   for (; got < 8; ++got) {
     const int flags = got == 7 ? (PyBUF_C_CONTIGUOUS | PyBUF_FORMAT | PyBUF_WRITABLE)
                                : (PyBUF_C_CONTIGUOUS | PyBUF_FORMAT);
     if (PyObject_GetBuffer(objs[got], &v[got], flags) != 0) goto fail;
     const int k = item_kind(&v[got]);
-    if (!k || (kind && k != kind)) {
+    if (k != kind) {
       ++got;
-      PyErr_SetString(PyExc_TypeError, "simulate buffers must all be float32 or all float64");
+      PyErr_SetString(PyExc_TypeError, "simulate buffers must all have the system precision's float type");
       goto fail;
     }
-    kind = k;
     const Py_ssize_t len = v[got].len / v[got].itemsize;
     if (got < 7) {
       if (n < 0) n = len;
@@ -107,7 +108,7 @@ fail:
 static PyMethodDef methods[] = {
     {"bind", bind, METH_VARARGS, "bind(addr_f32, addr_f64): nb_host_simulate_* of the loaded library"},
     {"simulate", simulate, METH_VARARGS,
-     "simulate(px, py, pz, m, vx, vy, vz, out6, g, dt, eps2, steps, device) -> C ABI status"},
+     "simulate(px, py, pz, m, vx, vy, vz, out6, g, dt, eps2, steps, device, itemsize) -> C ABI status"},
     {NULL, NULL, 0, NULL}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_hostpath", NULL, -1, methods,

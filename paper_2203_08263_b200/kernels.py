@@ -320,11 +320,12 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
     system (same class, layout and precision); ``sys_`` is not modified."""
     if variant is not None:
         _check(sys_, variant, None)
-    _check_buffers(sys_)
-    if params.steps < 1:
-        raise ValueError("steps must be >= 1")
     n, dtype = _count(sys_), _dtype(sys_)
-    if _distributed_world(group) > 1 or n < 1:
+    fast = n >= 1 and params.steps >= 1 and _distributed_world(group) <= 1
+    if not fast:
+        _check_buffers(sys_)
+        if params.steps < 1:
+            raise ValueError("steps must be >= 1")
         state = sys_.copy()
         pos, vel = simulate_arrays(_matrix(sys_, "positions"), _matrix(sys_, "velocities"), sys_.masses,
                                    params.softening_sq, params.dt, params.steps,
@@ -340,7 +341,11 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
     # columns and stores the final state straight into the pinned block) and
     # copied into one fresh 6*N result block; the kernel flags come from the
     # masses inside the call.
-    hp, device = _host_binding()
+    try:
+        hp, device = _host_binding()
+    except (RuntimeError, ImportError, AssertionError):
+        _check_buffers(sys_)  # a dtype mismatch is still the reference's ValueError, not a device error
+        raise
     soa = _value(sys_.layout) == "soa"
     if soa:
         (px, py, pz), (vx, vy, vz) = sys_.positions, sys_.velocities
@@ -348,8 +353,12 @@ def simulate(sys_, params, variant: Optional[KernelVariant] = None, group=None):
         px, py, pz, vx, vy, vz = (np.ascontiguousarray(c) for c in
                                   (*_columns(sys_, "positions"), *_columns(sys_, "velocities")))
     out = np.empty((6, n), dtype)
-    rc = hp.simulate(px, py, pz, sys_.masses, vx, vy, vz, out, params.gravitational_constant, params.dt,
-                     params.softening_sq, params.steps, device())
+    try:  # (the binding checks every buffer's item type against the precision)
+        rc = hp.simulate(px, py, pz, sys_.masses, vx, vy, vz, out, params.gravitational_constant, params.dt,
+                         params.softening_sq, params.steps, device(), dtype.itemsize)
+    except TypeError:
+        _check_buffers(sys_)  # the reference's dtype ValueError (_accel_cy.pyx:114)
+        raise
     if rc:
         from . import _native
         _native.check("nb_host_simulate", rc)

@@ -1,4 +1,5 @@
-"""simulate()'s single native call (nb_dev_simulate_cols) against the packed
+"""simulate()'s single native call (r02: the _hostpath binding into
+nb_host_simulate; the device-column call nb_dev_simulate_cols) against the packed
 device-state path (DeviceState.load + simulate + readback) on the same inputs:
 bitwise equal -- the small-N kernel reading and writing the host column block
 itself, and NB_FLAG_AUTO deriving the kernel flags from the staged masses in C
@@ -72,3 +73,47 @@ def test_nb_force_masks_overflowing_self_term(eps2, oracle):
     want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k].astype(np.float32)) for k in range(3)), s.masses,
                                 rows, 1.0, float(np.float32(eps2)))
     assert oracle.accel_dev(a[rows], want) <= 1e-4  # unsoftened: condition number is unbounded
+
+
+def test_binding_rejects_precision_mismatch_with_reference_error():
+    """On the GPU fast path the CPython binding checks every buffer's item type;
+    a mismatch surfaces as the reference's dtype ValueError (_accel_cy.pyx:114),
+    for a position column, a velocity column and the masses alike."""
+    for field in ("positions", "velocities", "masses"):
+        s = nb.uniform_cube(64, 1, nb.Precision.SINGLE)
+        if field == "masses":
+            s.masses = s.masses.astype(np.float64)
+        else:
+            cols = list(getattr(s, field))
+            cols[1] = cols[1].astype(np.float64)
+            setattr(s, field, tuple(cols))
+        with pytest.raises(ValueError, match="dtype mismatch"):
+            nb.simulate(s, nb.SimParams(1.0, 1e-3, 1e-3, 2))
+
+
+def test_simulate_result_columns_are_independent_and_input_untouched():
+    """The six result columns are disjoint views of one fresh block: writing one
+    changes no other, and the input system is not modified (simulate's
+    `state = sys_.copy()` contract, kernels/__init__.py:240)."""
+    s = nb.uniform_cube(500, 2, nb.Precision.DOUBLE)
+    before = [c.copy() for c in (*s.positions, *s.velocities, s.masses)]
+    fin = nb.simulate(s, nb.SimParams(1.0, 1e-2, 1e-2, 3))
+    for a, b in zip(before, (*s.positions, *s.velocities, s.masses)):
+        np.testing.assert_array_equal(a, b)
+    cols = (*fin.positions, *fin.velocities)
+    keep = [c.copy() for c in cols]
+    cols[0][:] = 7.0
+    for c, k in zip(cols[1:], keep[1:]):
+        np.testing.assert_array_equal(c, k)
+    assert all(c.flags["C_CONTIGUOUS"] and c.shape == (500,) for c in cols)
+    assert fin.masses is not s.masses
+
+
+def test_aos_simulate_equals_soa():
+    s = nb.uniform_cube(777, 4, nb.Precision.SINGLE)
+    aos = nb.convert_layout(s, nb.Layout.AOS)
+    p = nb.SimParams(1.0, 1e-3, 1e-3, 3)
+    a, b = nb.simulate(s, p), nb.simulate(aos, p)
+    assert b.layout is nb.Layout.AOS and b.positions.shape == (777, 3)
+    np.testing.assert_array_equal(a.position_matrix(), b.position_matrix())
+    np.testing.assert_array_equal(np.stack(a.velocities, 1), b.velocities)
