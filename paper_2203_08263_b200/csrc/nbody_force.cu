@@ -1089,6 +1089,12 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
 #ifndef NB_PAIR_TJ
 #define NB_PAIR_TJ 256
 #endif
+#ifndef NB_PAIR_SHFL
+// 1: the pair-interleaved tile copy by neighbour-lane shuffles (conflict-free
+// shared loads/stores); 0: each lane copies a source pair (32-byte stride, 2
+// wavefronts per access).
+#define NB_PAIR_SHFL 1
+#endif
 #ifndef NB_PAIR_UNROLL
 #define NB_PAIR_UNROLL 32
 #endif
@@ -1177,7 +1183,37 @@ __global__ void __cluster_dims__(PR_CL, 1, 1) __launch_bounds__(PR_T, 1) pair_ke
     if (more) issue(buf ^ 1, lo + TJ);  // buf^1 was released by the __syncwarp below
     const B* tb = tw + buf * TJ;
     const int count = (int)min((int64_t)TJ, s1 - lo);
-    if (Core::NEEDS_LM) {
+    if (Core::ODD && count == TJ) {
+      // Pair-interleaved copy of the tile for the odd target (and log2 m_j):
+      // lane l reads body j = l + 32i (contiguous 16-byte loads), swaps halves
+      // with its neighbour l^1 and writes ONE float4 -- (x0,x1,y0,y1) from the
+      // even lane, (z0,z1,m0,m1) from the odd one -- so loads and stores are
+      // conflict-free.
+      float4* ti = ilv + warp * TJ;
+#if NB_PAIR_SHFL
+#pragma unroll
+      for (int j = lane; j < TJ; j += 32) {
+        const B b = tb[j];
+        const float ox = __shfl_xor_sync(0xffffffffu, b.x, 1), oy = __shfl_xor_sync(0xffffffffu, b.y, 1);
+        const float oz = __shfl_xor_sync(0xffffffffu, b.z, 1), ow = __shfl_xor_sync(0xffffffffu, b.w, 1);
+        ti[j] = (lane & 1) ? make_float4(oz, b.z, ow, b.w) : make_float4(b.x, ox, b.y, oy);
+        if (Core::NEEDS_LM) lw[buf * TJ + j] = lg2_mufu(b.w);
+      }
+#else
+#pragma unroll 1
+      for (int p = lane; p < TJ / 2; p += 32) {
+        const B b0 = tb[2 * p], b1 = tb[2 * p + 1];
+        ti[2 * p] = make_float4(b0.x, b1.x, b0.y, b1.y);
+        ti[2 * p + 1] = make_float4(b0.z, b1.z, b0.w, b1.w);
+        if (Core::NEEDS_LM) {
+          lw[buf * TJ + 2 * p] = lg2_mufu(b0.w);
+          lw[buf * TJ + 2 * p + 1] = lg2_mufu(b1.w);
+        }
+      }
+#endif
+      __syncwarp();
+      core.tbi = ti;
+    } else if (Core::NEEDS_LM) {
       for (int r = lane; r < count; r += 32) lw[buf * TJ + r] = lg2_mufu(tb[r].w);
       __syncwarp();
     }
@@ -1194,17 +1230,6 @@ __global__ void __cluster_dims__(PR_CL, 1, 1) __launch_bounds__(PR_T, 1) pair_ke
     core.begin_tile();
     core.lmt = lw + buf * TJ;
     if (count == TJ) {
-      if constexpr (Core::ODD) {  // pair-interleaved copy of the tile for the odd target
-        float4* ti = ilv + warp * TJ;
-#pragma unroll
-        for (int p = lane; p < TJ / 2; p += 32) {
-          const B b0 = tb[2 * p], b1 = tb[2 * p + 1];
-          ti[2 * p] = make_float4(b0.x, b1.x, b0.y, b1.y);
-          ti[2 * p + 1] = make_float4(b0.z, b1.z, b0.w, b1.w);
-        }
-        __syncwarp();
-        core.tbi = ti;
-      }
       core.template full_tile<TJ>(tb);
     } else {
       int jj = 0;

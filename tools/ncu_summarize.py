@@ -42,8 +42,21 @@ def to_bytes(v, u):
     return v * scale
 summ_path = os.path.join(REPO, "profiles", "ncu_summary.json")
 summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
+# excess shared-memory wavefronts (bank conflicts that cost time) from the source page
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+srows = list(csv.reader(io.StringIO(src)))
+excess = None
+if len(srows) > 2 and "L1 Wavefronts Shared Excessive" in srows[1]:
+    sh = srows[1]
+    iw, iws = sh.index("L1 Wavefronts Shared Excessive"), sh.index("L1 Wavefronts Shared")
+    num = lambda v: float(v.replace(",", "")) if v not in ("", "-") else 0.0
+    excess = {"shared_wavefronts": sum(num(r[iws]) for r in srows[2:]),
+              "shared_wavefronts_excessive": sum(num(r[iw]) for r in srows[2:])}
 for name, ent in out.items():
-    if "step_kernel" in name:
+    if excess:
+        ent.update(excess)
+    if "step_kernel" in name or "pair_kernel" in name:
         dr = to_bytes(ent.get("dram__bytes_read.sum", 0), ent.get("dram__bytes_read.sum.unit", "byte"))
         dw = to_bytes(ent.get("dram__bytes_write.sum", 0), ent.get("dram__bytes_write.sum.unit", "byte"))
         summ[config] = {"kernel": name, "dram_bytes_per_launch": dr + dw, "metrics": ent,

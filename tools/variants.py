@@ -57,6 +57,8 @@ VARIANTS = {
     "pair_u12": {"NB_PAIR_UNROLL": 12},
     "pair_u32": {"NB_PAIR_UNROLL": 32},
     "pair_oddfirst": {"NB_PAIR_ODD_FIRST": 1},
+    "pair_shfl0": {"NB_PAIR_SHFL": 0},
+    "pair_shfl1": {"NB_PAIR_SHFL": 1},
     # small-N cooperative kernel with 12 / 16 warps per CTA (more latency hiding per SM)
     "small_t384": {"NB_SMALL_T": 384},
     "small_t512": {"NB_SMALL_T": 512},
