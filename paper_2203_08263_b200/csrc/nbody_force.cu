@@ -101,6 +101,12 @@
 // addressing, +6 MOVs per 16 sources; profiles/variants_r02_infix_pg.txt).
 #define NB_INFIX_DEFAULT 0
 #endif
+#ifndef NB_PAIR_ODD_EXP2
+// pair_kernel: every NB_PAIR_ODD_EXP2-th source pair of the odd target takes
+// the LG2/EX2 weight form (0: always the rsqrt form; 4 measured best of
+// 2/4/8/16: C2 -1.1 %, profiles/r02/pair_odd_exp2.log)
+#define NB_PAIR_ODD_EXP2 4
+#endif
 #ifndef NB_PAIR_ODD_FIRST
 #define NB_PAIR_ODD_FIRST 0  // pair_kernel: the odd target's source pair before (1) or after (0) the pairs'
 #endif
@@ -345,9 +351,20 @@ struct CoreF32 {
     d2 = fma2(dz, dz, d2);
     float d2a, d2b;
     upk(d2, d2a, d2b);
-    const f2x r = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
-    const f2x r2 = mul2(r, r);
-    f2x w = UNI ? mul2(r2, r) : mul2(mul2(r, ms), r2);
+    f2x w;
+    if (NB_PAIR_ODD_EXP2 && NB_F32_MATH == 0 && (p % NB_PAIR_ODD_EXP2) == 0) {
+      // this source pair's weights by 2^(-1.5 log2 d2 + log2 m) (LG2/EX2): XU work for FMA work
+      const f2x l = pk(lg2_mufu(d2a), lg2_mufu(d2b));
+      const f2x e = UNI ? mul2(l, pk(-1.5f, -1.5f))
+                        : fma2(l, pk(-1.5f, -1.5f), *reinterpret_cast<const f2x*>(lmt + 2 * p));
+      float ea, eb;
+      upk(e, ea, eb);
+      w = pk(ex2_mufu(ea), ex2_mufu(eb));
+    } else {
+      const f2x r = pk(rsqrt_mufu(d2a), rsqrt_mufu(d2b));
+      const f2x r2 = mul2(r, r);
+      w = UNI ? mul2(r2, r) : mul2(mul2(r, ms), r2);
+    }
     if (MASK) {
       float wa, wb;
       upk(w, wa, wb);

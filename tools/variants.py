@@ -59,6 +59,11 @@ VARIANTS = {
     "pair_oddfirst": {"NB_PAIR_ODD_FIRST": 1},
     "pair_shfl0": {"NB_PAIR_SHFL": 0},
     "pair_shfl1": {"NB_PAIR_SHFL": 1},
+    "pair_oddexp2_2": {"NB_PAIR_ODD_EXP2": 2},
+    "pair_oddexp2_4": {"NB_PAIR_ODD_EXP2": 4},
+    "pair_oddexp2_8": {"NB_PAIR_ODD_EXP2": 8},
+    "pair_oddexp2_16": {"NB_PAIR_ODD_EXP2": 16},
+    "pair_stagewise": {"NB_F32_STAGEWISE": 1},
     # small-N cooperative kernel with 12 / 16 warps per CTA (more latency hiding per SM)
     "small_t384": {"NB_SMALL_T": 384},
     "small_t512": {"NB_SMALL_T": 512},
