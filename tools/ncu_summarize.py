@@ -56,7 +56,7 @@ if len(srows) > 2 and "L1 Wavefronts Shared Excessive" in srows[1]:
 for name, ent in out.items():
     if excess:
         ent.update(excess)
-    if "step_kernel" in name or "pair_kernel" in name:
+    if "step_kernel" in name or "pair_kernel" in name or "simulate_kernel" in name:
         dr = to_bytes(ent.get("dram__bytes_read.sum", 0), ent.get("dram__bytes_read.sum.unit", "byte"))
         dw = to_bytes(ent.get("dram__bytes_write.sum", 0), ent.get("dram__bytes_write.sum.unit", "byte"))
         summ[config] = {"kernel": name, "dram_bytes_per_launch": dr + dw, "metrics": ent,
