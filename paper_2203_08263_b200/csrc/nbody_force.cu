@@ -1400,6 +1400,25 @@ __global__ void __launch_bounds__(T, MINB) simulate_kernel(StepArgs<typename Cor
 #ifndef NB_SMALL_T
 #define NB_SMALL_T 256
 #endif
+// Bytes of skew per source split of the small-N kernel's shared layout (FP64).
+template <typename R>
+__host__ __device__ constexpr int64_t small_split_skew() { return sizeof(R) == 8 ? 16 : 0; }
+// A staged body at a 16-byte-aligned shared address (FP64 bodies as two halves).
+__device__ __forceinline__ void st_body(unsigned char* p, const F4& b) { *reinterpret_cast<F4*>(p) = b; }
+__device__ __forceinline__ void st_body(unsigned char* p, const D4& b) {
+  double2* q = reinterpret_cast<double2*>(p);
+  q[0] = make_double2(b.x, b.y);
+  q[1] = make_double2(b.z, b.w);
+}
+template <typename B> __device__ __forceinline__ B ld_body(const unsigned char* p);
+template <> __device__ __forceinline__ F4 ld_body<F4>(const unsigned char* p) {
+  return *reinterpret_cast<const F4*>(p);
+}
+template <> __device__ __forceinline__ D4 ld_body<D4>(const unsigned char* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = q[0], b = q[1];
+  return D4{a.x, a.y, b.x, b.y};
+}
 constexpr int SN_T = NB_SMALL_T;  // threads per CTA (8 warps)
 
 // Bodies per split in shared memory: ceil(N/S) rounded up to 1 mod 8, so the
@@ -1429,8 +1448,14 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
   constexpr int S = (SN_T / 32) * G; // source splits per CTA
   constexpr int TB = 2 * PPW;        // target bodies per CTA
   extern __shared__ __align__(128) unsigned char sn_smem[];
-  B* sp = reinterpret_cast<B*>(sn_smem);                              // S * L bodies
-  float* slm = reinterpret_cast<float*>(sp + S * L);                  // log2(m_j), same layout
+  // S splits of L bodies, split-major (split s holds j = s, s+S, ...), each
+  // split SB bytes: FP64 splits carry a 16-byte skew so the 8 lane groups of a
+  // warp, which read 8 consecutive splits, and the staging stores of 8
+  // consecutive lanes fall in distinct 4-bank groups (conflict-free; 32-byte
+  // bodies at an L*32-byte split stride would pair up 2-way).
+  constexpr int64_t SKEW = small_split_skew<R>();
+  const int64_t SB = L * (int64_t)sizeof(B) + SKEW;
+  float* slm = reinterpret_cast<float*>(sn_smem + S * SB);            // log2(m_j) (FP32), slot() layout
   double* ssum = reinterpret_cast<double*>(slm + (Core::NEEDS_LM ? S * L : 0));
   double* red = ssum + Core::SMEM_SUMS * SN_T;                        // [8 warps][TB targets][3]
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
@@ -1441,6 +1466,7 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
   const int64_t n = a.n_all;
   const int64_t i0 = blockIdx.x * (int64_t)TB + 2 * pr;
   const int cnt = s < n ? (int)((n - s + S - 1) / S) : 0;
+  auto body_at = [&](int64_t j) { return sn_smem + (j % S) * SB + (j / S) * (int64_t)sizeof(B); };
   auto slot = [&](int64_t j) {
     const int64_t q = (j % S) * L + j / S;
     NB_DCHECK(j >= 0 && j < n && q >= 0 && q < S * L);
@@ -1493,7 +1519,7 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
       } else {
         b = ld4_cg(a.pos + j);
       }
-      sp[slot(j)] = b;
+      st_body(body_at(j), b);
       if (Core::NEEDS_LM) slm[slot(j)] = lg2_mufu((float)b.w);
     }
     __syncthreads();
@@ -1501,21 +1527,21 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
     tt[1] = gtimer();
 #endif
     const int64_t ia = i0 < n ? i0 : n - 1, ib = i0 + 1 < n ? i0 + 1 : n - 1;
-    core.set_pair(0, sp[slot(ia)], sp[slot(ib)]);
+    core.set_pair(0, ld_body<B>(body_at(ia)), ld_body<B>(body_at(ib)));
     core.zero_sums();
     core.begin_tile();
-    const B* tb = sp + s * L;
+    const unsigned char* tb = sn_smem + s * SB;
     NB_DCHECK(cnt >= 0 && cnt <= L);
     int jj = 0;
 #pragma unroll 1
     for (; jj + 4 <= cnt; jj += 4) {
-      core.interact(tb[jj], jj);
-      core.interact(tb[jj + 1], jj + 1);
-      core.interact(tb[jj + 2], jj + 2);
-      core.interact(tb[jj + 3], jj + 3);
+      core.interact(ld_body<B>(tb + jj * sizeof(B)), jj);
+      core.interact(ld_body<B>(tb + (jj + 1) * sizeof(B)), jj + 1);
+      core.interact(ld_body<B>(tb + (jj + 2) * sizeof(B)), jj + 2);
+      core.interact(ld_body<B>(tb + (jj + 3) * sizeof(B)), jj + 3);
     }
 #pragma unroll 1
-    for (; jj < cnt; ++jj) core.interact(tb[jj], jj);
+    for (; jj < cnt; ++jj) core.interact(ld_body<B>(tb + jj * sizeof(B)), jj);
     core.end_tile();
 #if NB_TRACE
     tt[2] = gtimer();
@@ -1547,9 +1573,9 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
       for (int w = 0; w < SN_T / 32; ++w)
 #pragma unroll
         for (int d = 0; d < 3; ++d) t[d] += red[(w * TB + tid) * 3 + d];
-      integrate_body<R>(a, il, t[0], t[1], t[2], vel, acc_prev, sp[slot(il)]);
+      integrate_body<R>(a, il, t[0], t[1], t[2], vel, acc_prev, ld_body<B>(body_at(il)));
       if (cols && st == last) {  // final state back into the columns (positions did not move in this step)
-        const B pf = sp[slot(il)];
+        const B pf = ld_body<B>(body_at(il));
         R* co = cols_out ? cols_out : cols;
         co[il] = pf.x;
         co[n + il] = pf.y;
@@ -1576,7 +1602,8 @@ int64_t small_smem_bytes(int64_t n, int ppw, bool needs_lm) {
   const int splits = (SN_T / 32) * (32 / ppw);
   const int64_t L = small_split_stride(n, splits);
   const int64_t sums = sizeof(R) == 4 ? 6 : 1;  // Core::SMEM_SUMS doubles per thread
-  return splits * L * (int64_t)sizeof(V4<R>) + (needs_lm ? splits * L * 4 : 0) + sums * SN_T * 8 +
+  return splits * (L * (int64_t)sizeof(V4<R>) + small_split_skew<R>()) + (needs_lm ? splits * L * 4 : 0) +
+         sums * SN_T * 8 +
          (SN_T / 32) * 2 * ppw * 3 * 8;
 }
 
