@@ -107,9 +107,6 @@
 // 2/4/8/16: C2 -1.1 %, profiles/r02/pair_odd_exp2.log)
 #define NB_PAIR_ODD_EXP2 4
 #endif
-#ifndef NB_PAIR_UNIFORM_WARP
-#define NB_PAIR_UNIFORM_WARP 0
-#endif
 #ifndef NB_PAIR_ODD_FIRST
 #define NB_PAIR_ODD_FIRST 0  // pair_kernel: the odd target's source pair before (1) or after (0) the pairs'
 #endif
@@ -1146,13 +1143,9 @@ __global__ void __cluster_dims__(PR_CL, 1, 1) __launch_bounds__(PR_T, 1) pair_ke
   uint64_t* bars = reinterpret_cast<uint64_t*>(sums + 3 * K * PR_T);               // [warp][2]
   cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
   const int tid = threadIdx.x, lane = tid & 31;
-#if NB_PAIR_UNIFORM_WARP
-  // the warp index through a shuffle: provably warp-uniform, so ptxas can keep
-  // the per-warp tile addresses in uniform registers (as the step kernel's)
-  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-#else
+  // (A warp index through __shfl_sync -- provably uniform, tile addresses in
+  // uniform registers as in the step kernel -- measured the same.)
   const int warp = tid >> 5;
-#endif
   const int rank = (int)cluster.block_rank();
   const int64_t blk = blockIdx.x / PR_CL;
   // this warp's slice [s0, s1) of the j range (multiples of 16 bodies but the end)
