@@ -1152,6 +1152,7 @@ __global__ void __cluster_dims__(PR_CL, 1, 1) __launch_bounds__(PR_T, 1) pair_ke
   const int64_t per = (a.j_count + PR_S * 16 - 1) / (PR_S * 16) * 16;
   const int sl = rank * PR_W + warp;
   const int64_t s0 = min(a.j_count, sl * per), s1 = min(a.j_count, s0 + per);
+  NB_DCHECK(blk * IBC < a.n_i && s0 >= 0 && s0 <= s1 && s1 <= a.j_count && rank < PR_CL);
   B* tw = tiles + warp * 2 * TJ;
   float* lw = lms + warp * 2 * TJ;
   uint64_t* bw = bars + warp * 2;
@@ -1188,6 +1189,7 @@ __global__ void __cluster_dims__(PR_CL, 1, 1) __launch_bounds__(PR_T, 1) pair_ke
       int64_t jg = a.j_begin + lo;
       if (jg >= a.n_all) jg -= a.n_all;
       const int64_t n1 = min(cnt, a.n_all - jg);
+      NB_DCHECK(cnt > 0 && cnt <= TJ && jg >= 0 && jg + n1 <= a.n_all && cnt - n1 <= a.n_all);
       mbar_expect_tx(bw + buf, (uint32_t)(cnt * sizeof(B)));
       bulk_g2s(tw + buf * TJ, a.pos + jg, (uint32_t)(n1 * sizeof(B)), bw + buf);
       if (cnt > n1) bulk_g2s(tw + buf * TJ + n1, a.pos, (uint32_t)((cnt - n1) * sizeof(B)), bw + buf);
@@ -1276,6 +1278,7 @@ __global__ void __cluster_dims__(PR_CL, 1, 1) __launch_bounds__(PR_T, 1) pair_ke
   for (int r = 0; r < PR_CL; ++r) part[r] = cluster.map_shared_rank(sums, r);
   for (int t = rank * (IBC / 2) + tid; t < (rank + 1) * (IBC / 2); t += PR_T) {
     const int k = t >> 5, l = t & 31;
+    NB_DCHECK(k < K && t < IBC);
     double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int s = 0; s < PR_S; ++s) {

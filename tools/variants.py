@@ -64,6 +64,7 @@ VARIANTS = {
     "pair_oddexp2_8": {"NB_PAIR_ODD_EXP2": 8},
     "pair_oddexp2_16": {"NB_PAIR_ODD_EXP2": 16},
     "pair_stagewise": {"NB_F32_STAGEWISE": 1},
+    "pair_tj128": {"NB_PAIR_TJ": 128},
     # small-N cooperative kernel with 12 / 16 warps per CTA (more latency hiding per SM)
     "small_t384": {"NB_SMALL_T": 384},
     "small_t512": {"NB_SMALL_T": 512},
