@@ -70,6 +70,19 @@
 #ifndef NB_F32_STAGEWISE
 #define NB_F32_STAGEWISE 0
 #endif
+#ifndef NB_F32_SPLIT_ACC
+// Experiment (0 = off, shipped): G > 0 runs a full tile in groups of G sources --
+// distances and weights of the group first, then, behind a scheduling boundary
+// (NB_F32_SPLIT_KIND 1: a warp barrier, 2: a single-trip loop ptxas cannot see
+// through), the group's accumulating FFMA2s in (source, pair, x/y/z) order, so the
+// three accumulates of a weight are adjacent and w comes from the operand reuse
+// cache (the accumulate is the one instruction with three distinct register
+// pairs; DESIGN 3.1.1).
+#define NB_F32_SPLIT_ACC 0
+#endif
+#ifndef NB_F32_SPLIT_KIND
+#define NB_F32_SPLIT_KIND 1
+#endif
 #ifndef NB_F32_EXP2_MASK
 // Which (target pair q, source phase p = jj mod NB_F32_EXP2_PHASES) weights go
 // through MUFU.LG2/EX2 instead of MUFU.RSQ + FMUL2s: bit q + (K/2)*p.  0 = none.
@@ -324,6 +337,10 @@ struct CoreF32 {
     e2s = eps2;
     ss = s;
     stride = st;
+#if NB_F32_SPLIT_ACC
+    one = st > 0 ? 1 : 0;  // st is a launch constant > 0; opaque to the compiler below
+    asm volatile("" : "+r"(one));
+#endif
   }
   __device__ __forceinline__ void set_pair(int q, const F4& p0, const F4& p1) {
     // +0 + (-x) is a real FADD2 (not an identity for x = +-0), so the pair is
@@ -404,11 +421,16 @@ struct CoreF32 {
   // accumulate -- the instruction with three distinct register pairs, which the
   // register file cannot feed at full rate -- gets the most reuse.
   __device__ __forceinline__ f2x weight(f2x d2, f2x mj, f2x lmj, int jj, int q) const {
+    return weight_p(d2, mj, lmj, jj, q, jj % NB_F32_EXP2_PHASES);
+  }
+  // phase: the source's LG2/EX2 phase (jj mod NB_F32_EXP2_PHASES, a compile-time
+  // value in the unrolled callers)
+  __device__ __forceinline__ f2x weight_p(f2x d2, f2x mj, f2x lmj, int jj, int q, int phase) const {
     float d2a, d2b;
     upk(d2, d2a, d2b);
     f2x w;
 #if NB_F32_MATH == 0
-    if ((XMASK >> (q + KP * (jj % NB_F32_EXP2_PHASES))) & 1u) {
+    if ((XMASK >> (q + KP * phase)) & 1u) {
       // m d2^(-3/2) = 2^(-1.5 log2 d2 + log2 m): one FFMA2 and four MUFU ops in
       // place of three FMUL2 + two MUFU.RSQ -- moves FP32-pipe work onto the XU
       // pipe, which the rsqrt form leaves ~40 % idle.
@@ -503,8 +525,66 @@ struct CoreF32 {
   // A full tile of TJ source bodies against the first NG pairs, unrolled
   // UNROLL_ deep.  (Software-pipelining stage A of body j+1 against stage B of
   // body j was measured slower: profiles/variants_r01_sweep2.txt, "pipe".)
+#if NB_F32_SPLIT_ACC
+  int one;  // 1 at run time (NB_F32_SPLIT_KIND 2: trip count of the boundary loops)
+  __device__ __forceinline__ void split_boundary() const {
+#if NB_F32_SPLIT_KIND == 1
+    __syncwarp();
+#endif
+  }
+  template <int TJ, int NG>
+  __device__ __forceinline__ void full_tile_split(const F4* tb) {
+    constexpr int G = NB_F32_SPLIT_ACC;
+    static_assert(TJ % G == 0 && G % NB_F32_EXP2_PHASES == 0, "group size");
+#pragma unroll(UNROLL_ / G > 0 ? UNROLL_ / G : 1)
+    for (int j0 = 0; j0 < TJ; j0 += G) {
+      f2x dx[G][NG], dy[G][NG], dz[G][NG], w[G][NG];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const F4 pj = tb[j0 + g];
+        const f2x xj = pk(pj.x, pj.x), yj = pk(pj.y, pj.y), zj = pk(pj.z, pj.z), mj = pk(pj.w, pj.w);
+        float lm = 0.f;
+        if (NEEDS_LM) lm = lmt[j0 + g];
+        const f2x lmj = pk(lm, lm);
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+          dx[g][q] = add2(xj, nx[q]);
+          dy[g][q] = add2(yj, ny[q]);
+          dz[g][q] = add2(zj, nz[q]);
+          f2x d2 = fma2(dx[g][q], dx[g][q], e2);
+          d2 = fma2(dy[g][q], dy[g][q], d2);
+          d2 = fma2(dz[g][q], dz[g][q], d2);
+          w[g][q] = weight_p(d2, mj, lmj, j0 + g, q, g % NB_F32_EXP2_PHASES);
+        }
+      }
+      split_boundary();
+#if NB_F32_SPLIT_KIND == 2
+#pragma unroll 1
+      for (int r = 0; r < one; ++r)
+#endif
+      {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+#pragma unroll
+          for (int q = 0; q < NG; ++q) {
+            tx[q] = fma2(w[g][q], dx[g][q], tx[q]);
+            ty[q] = fma2(w[g][q], dy[g][q], ty[q]);
+            tz[q] = fma2(w[g][q], dz[g][q], tz[q]);
+          }
+        }
+      }
+      split_boundary();
+    }
+  }
+#endif
   template <int TJ, int NG = KP>
   __device__ __forceinline__ void full_tile(const F4* tb) {
+#if NB_F32_SPLIT_ACC
+    if constexpr (!ODD) {
+      full_tile_split<TJ, NG>(tb);
+      return;
+    }
+#endif
     if constexpr (ODD && NG == KP) {
       // every source read from the pair-interleaved tile (tbi): the pairs'
       // broadcast bodies and the odd target's packed source pair alike
@@ -889,6 +969,9 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
   }
   Core core;
   core.init(a.eps2, s_sums + tid, T);
+#if NB_F32_SPLIT_ACC
+  if constexpr (sizeof(R) == 4) core.one = (int)(a.n_all >> 40) + 1;  // 1, from a kernel parameter: opaque to ptxas
+#endif
   uint32_t phase_bits = 0u;  // mbarrier phase parity of tile buffer b in bit b (TMA staging)
   __shared__ float tile_lm[2][Core::NEEDS_LM ? TJ : 1];  // log2(m_j) of the staged tiles
 

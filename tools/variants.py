@@ -68,6 +68,13 @@ VARIANTS = {
     # small-N cooperative kernel with 12 / 16 warps per CTA (more latency hiding per SM)
     "small_t384": {"NB_SMALL_T": 384},
     "small_t512": {"NB_SMALL_T": 512},
+    # round 2: accumulating FFMA2s of a group of G sources behind a loop boundary
+    # (triples adjacent: w from the operand reuse cache), NB_F32_SPLIT_ACC = G
+    "split2": {"NB_F32_SPLIT_ACC": 2, "NB_F32_SPLIT_KIND": 2},
+    "split4": {"NB_F32_SPLIT_ACC": 4, "NB_F32_SPLIT_KIND": 2},
+    "split8": {"NB_F32_SPLIT_ACC": 8, "NB_F32_SPLIT_KIND": 2},
+    "split4_u8": {"NB_F32_SPLIT_ACC": 4, "NB_F32_SPLIT_KIND": 2, "NB_F32_UNROLL": 8},
+    "split4_u4": {"NB_F32_SPLIT_ACC": 4, "NB_F32_SPLIT_KIND": 2, "NB_F32_UNROLL": 4},
     # extra nvcc flags per variant: {"_flags": ["-Xptxas", "..."]}
 }
 
