@@ -83,6 +83,9 @@
 #ifndef NB_F32_SPLIT_KIND
 #define NB_F32_SPLIT_KIND 1
 #endif
+#ifndef NB_F64_SPLIT_ACC
+#define NB_F64_SPLIT_ACC 0  // the same experiment for the FP64 core's accumulating DFMAs (G sources per group)
+#endif
 #ifndef NB_F32_EXP2_MASK
 // Which (target pair q, source phase p = jj mod NB_F32_EXP2_PHASES) weights go
 // through MUFU.LG2/EX2 instead of MUFU.RSQ + FMUL2s: bit q + (K/2)*p.  0 = none.
@@ -640,7 +643,12 @@ struct CoreF64 {
   int selfj[K];
   double e2;
 
-  __device__ __forceinline__ void init(double eps2, double*, int) { e2 = eps2; }
+  __device__ __forceinline__ void init(double eps2, double*, int) {
+    e2 = eps2;
+#if NB_F64_SPLIT_ACC
+    one = 1;
+#endif
+  }
   __device__ __forceinline__ void set_pair(int q, const D4& p0, const D4& p1) {
     nx[2 * q] = -p0.x; ny[2 * q] = -p0.y; nz[2 * q] = -p0.z;
     nx[2 * q + 1] = -p1.x; ny[2 * q + 1] = -p1.y; nz[2 * q + 1] = -p1.z;
@@ -656,10 +664,54 @@ struct CoreF64 {
   __device__ __forceinline__ void begin_tile() {}
   __device__ __forceinline__ void end_tile() {}
   static constexpr int KG = K / 2;  // target groups (pairs) per thread, as in the FP32 core
+#if NB_F64_SPLIT_ACC
+  int one;  // 1 at run time, from a kernel parameter (trip count of the boundary loop)
+#endif
   template <int TJ, int NG = KG>
   __device__ __forceinline__ void full_tile(const D4* tb) {
+#if NB_F64_SPLIT_ACC
+    constexpr int G = NB_F64_SPLIT_ACC, NK = 2 * NG;
+    static_assert(TJ % G == 0, "group size");
+#pragma unroll(UNROLL_ / G > 0 ? UNROLL_ / G : 1)
+    for (int j0 = 0; j0 < TJ; j0 += G) {
+      double dx[G][NK], dy[G][NK], dz[G][NK], w[G][NK];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const D4 pj = tile_get<TJ>(tb, j0 + g);
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          dx[g][k] = pj.x + nx[k];
+          dy[g][k] = pj.y + ny[k];
+          dz[g][k] = pj.z + nz[k];
+          double d2 = fma(dx[g][k], dx[g][k], e2);
+          d2 = fma(dy[g][k], dy[g][k], d2);
+          d2 = fma(dz[g][k], dz[g][k], d2);
+          const double y = rsqrt_seed(d2);
+          const double t = y * y;
+          const double e = fma(-d2, t, 1.0);
+          const double my3 = UNI ? t * y : pj.w * (t * y);
+          const double q = F64_CORR(e);
+          w[g][k] = fma(my3, q, my3);
+          if (MASK && j0 + g == selfj[k]) w[g][k] = 0.0;
+        }
+      }
+#pragma unroll 1
+      for (int r = 0; r < one; ++r) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+#pragma unroll
+          for (int k = 0; k < NK; ++k) {
+            sx[k] = fma(w[g][k], dx[g][k], sx[k]);
+            sy[k] = fma(w[g][k], dy[g][k], sy[k]);
+            sz[k] = fma(w[g][k], dz[g][k], sz[k]);
+          }
+        }
+      }
+    }
+#else
 #pragma unroll UNROLL_
     for (int jj = 0; jj < TJ; ++jj) interact_g<NG>(tile_get<TJ>(tb, jj), jj);
+#endif
   }
   __device__ __forceinline__ void interact(const D4& pj, int jj) { interact_g<KG>(pj, jj); }
   // One source body against the first 2*NG targets (the rest are dead rows of a
@@ -971,6 +1023,9 @@ __device__ __forceinline__ void step_body(const StepArgs<typename Core::R>& a,
   core.init(a.eps2, s_sums + tid, T);
 #if NB_F32_SPLIT_ACC
   if constexpr (sizeof(R) == 4) core.one = (int)(a.n_all >> 40) + 1;  // 1, from a kernel parameter: opaque to ptxas
+#endif
+#if NB_F64_SPLIT_ACC
+  if constexpr (sizeof(R) == 8) core.one = (int)(a.n_all >> 40) + 1;
 #endif
   uint32_t phase_bits = 0u;  // mbarrier phase parity of tile buffer b in bit b (TMA staging)
   __shared__ float tile_lm[2][Core::NEEDS_LM ? TJ : 1];  // log2(m_j) of the staged tiles

@@ -75,6 +75,9 @@ VARIANTS = {
     "split8": {"NB_F32_SPLIT_ACC": 8, "NB_F32_SPLIT_KIND": 2},
     "split4_u8": {"NB_F32_SPLIT_ACC": 4, "NB_F32_SPLIT_KIND": 2, "NB_F32_UNROLL": 8},
     "split4_u4": {"NB_F32_SPLIT_ACC": 4, "NB_F32_SPLIT_KIND": 2, "NB_F32_UNROLL": 4},
+    "f64_split1": {"NB_F64_SPLIT_ACC": 1},
+    "f64_split2": {"NB_F64_SPLIT_ACC": 2},
+    "f64_split4": {"NB_F64_SPLIT_ACC": 4},
     # extra nvcc flags per variant: {"_flags": ["-Xptxas", "..."]}
 }
 
