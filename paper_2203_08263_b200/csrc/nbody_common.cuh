@@ -58,6 +58,45 @@ __device__ __forceinline__ void st4(D4* p, D4 v) {
   q[1] = make_double2(v.z, v.w);
 }
 
+// Single-transaction, gpu-coherent accesses of one packed body: 128 bits (FP32)
+// or 256 bits (FP64, LDG/STG.E.ENL2.256 on sm_100a) in ONE relaxed gpu-scope
+// access of an aligned 16- / 32-byte record, i.e. at most one 32-byte sector, so
+// a reader sees a record entirely old or entirely new.  The small-N kernel's
+// tagged position exchange rests on that: the record's fourth word carries the
+// step tag, and no other data is consumed under it.
+__device__ __forceinline__ F4 ld4_pub(const F4* p) {
+  F4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ D4 ld4_pub(const D4* p) {
+  D4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st4_pub(F4* p, F4 v) {
+  asm volatile("st.relaxed.gpu.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st4_pub(D4* p, D4 v) {
+  asm volatile("st.relaxed.gpu.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+               : "memory");
+}
+// Step tag <-> the bit pattern of a body's fourth word.  Sign bit set: never the
+// pattern of a valid (positive, finite) mass.  No arithmetic touches the word.
+__device__ __forceinline__ float tag_word(float, unsigned long long t) {
+  return __uint_as_float(0x80000000u | (unsigned)(t & 0x7fffffffull));
+}
+__device__ __forceinline__ double tag_word(double, unsigned long long t) {
+  return __longlong_as_double((long long)(0x8000000000000000ull | (t & 0x7fffffffffffffffull)));
+}
+__device__ __forceinline__ bool same_word(float a, float b) { return __float_as_uint(a) == __float_as_uint(b); }
+__device__ __forceinline__ bool same_word(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
 // ---------------------------------------------------------------- exact IEEE ops
 // The integrator must reproduce the reference's rounding sequence bit for bit
 // (pkg/setup.py:7-8,17 builds with -ffp-contract=off), so every update op is an

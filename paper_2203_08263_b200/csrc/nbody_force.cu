@@ -801,7 +801,8 @@ __device__ __forceinline__ void integrate_body(const StepArgs<R>& a, int64_t il,
       p.y = add_rn(p.y, mul_rn(add_rn(v.y, mul_rn(a.half, dvy)), a.dt));
       p.z = add_rn(p.z, mul_rn(add_rn(v.z, mul_rn(a.half, dvz)), a.dt));
       NB_DCHECK(ig >= 0 && ig < a.n_all && il >= 0 && il < a.n_i);
-      st4(a.pos_next + ig, p);
+      if (a.pub) st4_pub(a.pos_next + ig, p);
+      else st4(a.pos_next + ig, p);
       for (int q = 0; q < a.n_peers; ++q) st4(a.peers[q] + ig, p);  // NVLink peer stores
       v.x = add_rn(v.x, dvx);
       v.y = add_rn(v.y, dvy);
@@ -1544,6 +1545,16 @@ __device__ __forceinline__ void st_body(unsigned char* p, const D4& b) {
   q[0] = make_double2(b.x, b.y);
   q[1] = make_double2(b.z, b.w);
 }
+// Position only: the staged body's mass (fourth word) stays as step 0 left it.
+__device__ __forceinline__ void st_body_xyz(unsigned char* p, const F4& b) {
+  *reinterpret_cast<float2*>(p) = make_float2(b.x, b.y);
+  reinterpret_cast<float*>(p)[2] = b.z;
+}
+__device__ __forceinline__ void st_body_xyz(unsigned char* p, const D4& b) {
+  double2* q = reinterpret_cast<double2*>(p);
+  q[0] = make_double2(b.x, b.y);
+  reinterpret_cast<double*>(p)[2] = b.z;
+}
 template <typename B> __device__ __forceinline__ B ld_body(const unsigned char* p);
 template <> __device__ __forceinline__ F4 ld_body<F4>(const unsigned char* p) {
   return *reinterpret_cast<const F4*>(p);
@@ -1639,22 +1650,57 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
     a.pos_next = (st & 1) ? pos_a : pos_b;
     // step 0 of a column-block run: the packed buffer holds no state yet
     a.mass0 = (cols && st == 0) ? cols + 3 * n : nullptr;
+    // Tagged exchange (a.tag != 0): the drift of step st stores every body as one
+    // coherent record whose fourth word is the tag of step st+1 instead of the
+    // mass, and step st+1 stages by polling each record until it carries that
+    // tag -- the staging read IS the grid-wide wait (one L2 round trip in place
+    // of barrier + read).  Masses and log2 m stay in shared memory from step 0.
+    // Buffer reuse is safe: a CTA overwrites buffer b (tag st+2) only after it
+    // saw every record of the other buffer tagged st+1, and a CTA publishes
+    // those only after it finished staging buffer b.  The first and the last
+    // drift (st = 0, steps-1) store real masses and are followed by the grid
+    // barrier: a polled buffer then never holds anything but masses (sign bit
+    // clear) or this launch's own earlier tags -- no stale data of another launch
+    // or process can match -- and the launch leaves the current buffer as every
+    // other kernel expects it.
+    const bool tagged_out = a.tag != 0 && st >= 1 && st < steps - 1;     // this step's drift publishes tags
+    const bool tagged_in = a.tag != 0 && st >= 2 && st <= steps - 1;     // this step's staging polls them
+    a.pub = tagged_out ? 1 : 0;
 #if NB_TRACE
     unsigned long long tt[5];
     tt[0] = gtimer();
 #endif
-    for (int64_t j = tid; j < n; j += SN_T) {  // positions moved last step: coherent loads
-      B b;
-      if (cols && st == 0) {
-        b.x = cols[j];
-        b.y = cols[n + j];
-        b.z = cols[2 * n + j];
-        b.w = cols[3 * n + j];
-      } else {
-        b = ld4_cg(a.pos + j);
+    if (tagged_in) {
+      const R want = tag_word(R(0), a.tag + (unsigned long long)st);
+      if (a.uniform_mass) a.mass0 = reinterpret_cast<const R*>(body_at(0)) + 3;  // a.pos[0].w is a tag
+      for (int64_t j0 = tid; j0 < n; j0 += 4 * SN_T) {
+        B b[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (j0 + r * SN_T < n) b[r] = ld4_pub(a.pos + j0 + r * SN_T);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int64_t j = j0 + r * SN_T;
+          if (j < n) {
+            while (!same_word(b[r].w, want)) b[r] = ld4_pub(a.pos + j);
+            st_body_xyz(body_at(j), b[r]);
+          }
+        }
       }
-      st_body(body_at(j), b);
-      if (Core::NEEDS_LM) slm[slot(j)] = lg2_mufu((float)b.w);
+    } else {
+      for (int64_t j = tid; j < n; j += SN_T) {  // positions moved last step: coherent loads
+        B b;
+        if (cols && st == 0) {
+          b.x = cols[j];
+          b.y = cols[n + j];
+          b.z = cols[2 * n + j];
+          b.w = cols[3 * n + j];
+        } else {
+          b = ld4_cg(a.pos + j);
+        }
+        st_body(body_at(j), b);
+        if (Core::NEEDS_LM) slm[slot(j)] = lg2_mufu((float)b.w);
+      }
     }
     __syncthreads();
 #if NB_TRACE
@@ -1707,7 +1753,9 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
       for (int w = 0; w < SN_T / 32; ++w)
 #pragma unroll
         for (int d = 0; d < 3; ++d) t[d] += red[(w * TB + tid) * 3 + d];
-      integrate_body<R>(a, il, t[0], t[1], t[2], vel, acc_prev, ld_body<B>(body_at(il)));
+      B pcur = ld_body<B>(body_at(il));
+      if (tagged_out) pcur.w = tag_word(R(0), a.tag + (unsigned long long)st + 1);
+      integrate_body<R>(a, il, t[0], t[1], t[2], vel, acc_prev, pcur);
       if (cols && st == last) {  // final state back into the columns (positions did not move in this step)
         const B pf = ld_body<B>(body_at(il));
         R* co = cols_out ? cols_out : cols;
@@ -1723,7 +1771,11 @@ __global__ void __launch_bounds__(SN_T) small_simulate_kernel(StepArgs<typename 
     __syncthreads();
     tt[3] = gtimer();
 #endif
-    if (st < steps) grid.sync();  // new positions visible; nobody still reads the old buffer, sp or red
+    // new positions visible; nobody still reads the old buffer, sp or red
+    if (st < steps) {
+      if (tagged_out) __syncthreads();  // (the next staging's tag poll is the grid-wide wait)
+      else grid.sync();
+    }
 #if NB_TRACE
     tt[4] = gtimer();
     trace_put(6, (unsigned long long)blockIdx.x | ((unsigned long long)st << 32), tt, 5);
@@ -1869,6 +1921,13 @@ static unsigned long long next_tag() {
     return ((unsigned long long)rd() << 32 | rd()) & 0xffffff0000000000ull;
   }();
   return salt | ((counter.fetch_add(1) + 1) & 0xffffffffffull);
+}
+
+// n consecutive tag values no earlier launch of this process was given (the
+// small-N kernel's per-step record tags): tag, tag+1, ... tag+n-1, never 0.
+static unsigned long long reserve_tags(unsigned long long n) {
+  static std::atomic<unsigned long long> next{1};
+  return next.fetch_add(n);
 }
 
 // Resident CTAs per SM x SMs for a kernel (cached): the most CTAs that can be
@@ -2130,7 +2189,10 @@ static const void* small_fn(bool mask_self, bool uni) {
 }
 
 // 8 targets per CTA (twice the CTAs) up to N = 3072 (FP32) / 1184 (FP64), else
-// 16: the measured crossovers (profiles/small_n_r01.md; NB_SMALL_PPW=4|8 forces one).
+// 16: the measured crossovers (profiles/small_n_r01.md; NB_SMALL_PPW=4|8 forces
+// one).  When the 8-target grid exceeds what is co-resident (FP32 above N = 2368
+// at 2 CTAs per SM), the 16-target form is taken instead of falling back to the
+// stream-K paths.
 template <typename R>
 cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>* pos_b, int64_t steps,
                                   cudaStream_t stream, R* cols, R* cols_out) {
@@ -2138,12 +2200,14 @@ cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>*
   a.uniform_mass = uni ? 1 : 0;
   const int64_t n = a.n_all;
   NB_HT(10);
-  int ppw = n <= (sizeof(R) == 4 ? 3072 : 1184) ? 4 : 8;
-  if (const char* env = getenv("NB_SMALL_PPW")) ppw = atoi(env) == 4 ? 4 : 8;  // (read per call: tools/small_n_bench.py)
-  const void* fn = ppw == 4 ? small_fn<R, 4>(mask_self, uni) : small_fn<R, 8>(mask_self, uni);
+  int first = n <= (sizeof(R) == 4 ? 3072 : 1184) ? 4 : 8;
+  bool forced = false;
+  if (const char* env = getenv("NB_SMALL_PPW")) {  // (read per call: tools/small_n_bench.py)
+    first = atoi(env) == 4 ? 4 : 8;
+    forced = true;
+  }
   bool needs_lm = false;
   if constexpr (sizeof(R) == 4) needs_lm = !uni && SmallF32<false, false>::NEEDS_LM;
-  const int64_t smem = small_smem_bytes<R>(n, ppw, needs_lm);
   // Host-side launch preparation is on simulate()'s critical path at small N:
   // the co-resident capacity is cached per (device, kernel, shared-memory size)
   // and the opt-in shared-memory limit per (device, kernel) only ever raised.
@@ -2153,35 +2217,62 @@ cudaError_t launch_simulate_small(StepArgs<R> a, int flags, V4<R>* pos_a, V4<R>*
   static Opt opts[32];
   static int n_caps = 0, n_opts = 0;
   static std::mutex mu;  // host threads may launch concurrently on different streams
-  std::unique_lock<std::mutex> lock(mu);
-  int dev = 0;
-  cudaGetDevice(&dev);
-  Opt* opt = nullptr;
-  for (int k = 0; k < n_opts; ++k)
-    if (opts[k].dev == dev && opts[k].fn == fn) opt = &opts[k];
-  if (!opt || opt->smem < smem) {
-    int smem_max = 0;
-    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (smem > smem_max) return cudaErrorCooperativeLaunchTooLarge;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    if (!opt && n_opts < 32) opt = &opts[n_opts++];
-    if (opt) *opt = Opt{dev, fn, smem};
+  int ppw = first;
+  const void* fn = nullptr;
+  int64_t smem = 0, grid = 0;
+  for (;;) {
+    fn = ppw == 4 ? small_fn<R, 4>(mask_self, uni) : small_fn<R, 8>(mask_self, uni);
+    smem = small_smem_bytes<R>(n, ppw, needs_lm);
+    grid = (n + 2 * ppw - 1) / (2 * ppw);
+    std::unique_lock<std::mutex> lock(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Opt* opt = nullptr;
+    for (int k = 0; k < n_opts; ++k)
+      if (opts[k].dev == dev && opts[k].fn == fn) opt = &opts[k];
+    cudaError_t fit = cudaSuccess;
+    if (!opt || opt->smem < smem) {
+      int smem_max = 0;
+      cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      if (smem > smem_max) {
+        fit = cudaErrorCooperativeLaunchTooLarge;
+      } else {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        if (!opt && n_opts < 32) opt = &opts[n_opts++];
+        if (opt) *opt = Opt{dev, fn, smem};
+      }
+    }
+    if (fit == cudaSuccess) {
+      int capacity = -1;
+      for (int k = 0; k < n_caps; ++k)
+        if (caps[k].dev == dev && caps[k].fn == fn && caps[k].smem == smem) capacity = caps[k].capacity;
+      if (capacity < 0) {
+        int per_sm = 0, sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SN_T, (size_t)smem);
+        capacity = per_sm * sms;
+        if (n_caps < 64) caps[n_caps++] = Cap{dev, fn, smem, capacity};
+      }
+      if (grid > (int64_t)capacity) fit = cudaErrorCooperativeLaunchTooLarge;
+    }
+    lock.unlock();
+    if (fit == cudaSuccess) break;
+    if (ppw == 4 && !forced) {
+      ppw = 8;  // half the CTAs
+      continue;
+    }
+    return fit;
   }
-  int capacity = -1;
-  for (int k = 0; k < n_caps; ++k)
-    if (caps[k].dev == dev && caps[k].fn == fn && caps[k].smem == smem) capacity = caps[k].capacity;
-  if (capacity < 0) {
-    int per_sm = 0, sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SN_T, (size_t)smem);
-    capacity = per_sm * sms;
-    if (n_caps < 64) caps[n_caps++] = Cap{dev, fn, smem, capacity};
-  }
-  lock.unlock();
   NB_HT(11);
-  const int64_t grid = (n + 2 * ppw - 1) / (2 * ppw);
-  if (grid > (int64_t)capacity) return cudaErrorCooperativeLaunchTooLarge;
+  // Tagged position exchange between steps (NB_SMALL_TAGGED=0: a grid barrier
+  // per step): steps+1 consecutive tags no earlier launch used.
+  static const bool tagged = [] {
+    const char* e = getenv("NB_SMALL_TAGGED");
+    return !e || atoi(e) != 0;
+  }();
+  a.tag = (tagged && steps >= 3) ? reserve_tags((unsigned long long)steps + 1) : 0;
+  a.pub = 0;
   int64_t L = small_split_stride(n, (SN_T / 32) * (32 / ppw));
   void* args[] = {&a, &pos_a, &pos_b, &steps, &L, &cols, &cols_out};
   NB_HT(12);

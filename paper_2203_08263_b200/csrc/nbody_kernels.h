@@ -51,6 +51,9 @@ struct StepArgs {
   // set to this launch's unique tag once the slot's partials are visible.
   unsigned long long* flags;
   unsigned long long tag;
+  // 1: the drifted body is stored with ONE coherent 128-/256-bit access (st4_pub):
+  // the small-N kernel's tagged position exchange (its fourth word is the step tag)
+  int pub;
   int64_t units, n_tiles, n_iblocks;
   int64_t grid;
   // Cost-balanced stream-K (Sched in nbody_force.cu): target groups per thread
