@@ -29,10 +29,12 @@
 //    fixup_kernel (programmatic dependent launch, 32-thread CTAs) in fixed CTA
 //    order -- bitwise reproducible run to run -- which then runs the epilogue.
 //  * NB_TRACE builds record per-CTA %globaltimer timelines (tools/trace_launches.py).
-//  * Small N: the whole multi-step loop runs in one cooperative launch with a
-//    grid barrier per step -- small_simulate_kernel (N <= 4096 FP32 / 2560 FP64:
-//    source split inside the CTA, no global partials) or simulate_kernel (up to
-//    8192: the stream-K decomposition, bitwise identical to per-step launches).
+//  * Small N: the whole multi-step loop runs in one cooperative launch --
+//    small_simulate_kernel (N <= 4096 FP32 / 2560 FP64: source split inside the
+//    CTA, no global partials; between its first and last step the positions are
+//    exchanged as tagged coherent records, the staging poll standing in for the
+//    grid barrier) or simulate_kernel (up to 8192: the stream-K decomposition
+//    with a grid barrier per step, bitwise identical to per-step launches).
 #include "nbody_common.cuh"
 #include "nbody_kernels.h"
 
