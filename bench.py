@@ -540,12 +540,15 @@ def run_ours(args) -> dict:
         nb.simulate(sys_host, params)
         per_call = time.perf_counter() - tw
         calls = max(args.steps, min(5000, int(0.2 / max(per_call, 1e-6)) + 1))
-        for _ in range(calls if calls > args.steps else 0):
-            nb.simulate(sys_host, params)
-        if world > 1:  # every rank runs the same number of calls
+        if world > 1:
+            # every rank runs the same number of calls -- agreed BEFORE the extra
+            # warm-up calls: a sharded simulate is a collective, so ranks whose own
+            # timings gave different counts would otherwise leave it mismatched
             t = torch.tensor([calls], dtype=torch.int64, device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             calls = int(t.item())
+        for _ in range(calls if calls > args.steps else 0):
+            nb.simulate(sys_host, params)
         barrier()
         t0 = time.perf_counter()
         final = None
