@@ -226,7 +226,9 @@ int dev_simulate(void* pos_a, void* pos_b, void* vel4, void* acc4, int64_t n, do
     NB_CUDA(launch_pack_soa<R>(cols, cols + n, cols + 2 * n, cols + 3 * n, static_cast<V4<R>*>(pos_a), n, st));
     NB_CUDA(launch_pack_soa<R>(cols + 4 * n, cols + 5 * n, cols + 6 * n, nullptr, static_cast<V4<R>*>(vel4), n, st));
   }
-  if (!events && n <= persistent_max_n()) {
+  // (FP32 sizes the cluster split-source kernel covers go per step: it has no
+  // partial slots, fixup pass or grid barriers to pay per step.)
+  if (!events && n <= persistent_max_n() && strcmp(step_kernel_name<R>(n, n), "pair_kernel") != 0) {
     // small N: the whole loop in one cooperative launch (launch-bound otherwise)
     StepArgs<R> a;
     int rc = make_step_args<R>(a, pos_a, n, 0, n, 0, n, g, eps2, dt, NB_STEP_FIRST, flags, nullptr, 0, acc4, vel4,

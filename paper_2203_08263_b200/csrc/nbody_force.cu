@@ -1241,8 +1241,14 @@ __global__ void __launch_bounds__(T, MINB) step_kernel(const StepArgs<typename C
 // CTA's through distributed shared memory, and CTA r runs the epilogue of half
 // r of the i-block: no partial slots, no fixup launch, bitwise reproducible.
 // With 74 clusters on 148 SMs, K = 7 covers N <= 16576 (C2: 1.2 % dead lanes).
+// The kernel is instantiated for K = NB_PAIR_KMIN .. NB_PAIR_K targets per lane
+// (74 * 32 * K target slots: 4736, 7104, 9472, 11840, 14208, 16576) and a launch
+// takes the smallest K that holds its targets (pair_clusters).
 #ifndef NB_PAIR_K
 #define NB_PAIR_K 7
+#endif
+#ifndef NB_PAIR_KMIN
+#define NB_PAIR_KMIN 2
 #endif
 #ifndef NB_PAIR_TJ
 #define NB_PAIR_TJ 256
@@ -1261,7 +1267,7 @@ constexpr int PR_W = PR_T / 32;       // warps = source slices per CTA
 constexpr int PR_CL = 2;              // CTAs per cluster
 constexpr int PR_S = PR_W * PR_CL;    // source slices per i-block
 
-template <bool M, bool U> struct CorePair : CoreF32<NB_PAIR_K, M, NB_PAIR_UNROLL, U> {
+template <int K, bool M, bool U> struct CorePair : CoreF32<K, M, NB_PAIR_UNROLL, U> {
   static constexpr bool MASK_SELF = M;
 };
 
@@ -2012,22 +2018,34 @@ static int sm_count() {
   return sms;
 }
 
-// Clusters of an FP32 launch through pair_kernel, 0 for the stream-K path: its
-// i-blocks fill one wave of 2-CTA clusters with <= 6 % dead target lanes and
-// every warp's source slice holds at least one full tile.  NB_PAIR=0 / 1 turns
-// it off / on wherever the i-blocks fit one wave (A/B measurements).
-static int pair_clusters(int64_t n_i, int64_t j_count) {
+// Clusters of an FP32 launch through pair_kernel (0: the stream-K path) and its
+// targets per lane K: the smallest K whose one wave of 2-CTA clusters (74 * 32 * K
+// target slots on 148 SMs) holds the launch's targets, taken when the slots are
+// filled at least to the measured break-even against the stream-K / persistent
+// paths (profiles/r02/pair_kfam.txt: K <= 4 wins over its whole range, K = 5, 6,
+// 7 from 88.7 / 90 / 92.7 %: K = 7 from 15367 targets, where stream-K needs its 11th i-block) and every warp's source slice holds at least one
+// full tile.  NB_PAIR=0 / 1 turns it off / on wherever the targets fit one wave
+// (A/B measurements, tests).
+static int pair_clusters(int64_t n_i, int64_t j_count, int* k_out = nullptr) {
   static int env = -2;
   if (env == -2) {
     const char* e = getenv("NB_PAIR");
     env = e ? atoi(e) : -1;
   }
   if (env == 0 || n_i < 1) return 0;
-  constexpr int64_t IBC = 32 * NB_PAIR_K;
   const int64_t waves = sm_count() / PR_CL;
-  const int64_t ncl = (n_i + IBC - 1) / IBC;
+  int64_t k = (n_i + waves * 32 - 1) / (waves * 32);
+  if (k < NB_PAIR_KMIN) k = NB_PAIR_KMIN;
+  if (k > NB_PAIR_K) return 0;
+  const int64_t ibc = 32 * k;
+  const int64_t ncl = (n_i + ibc - 1) / ibc;
   if (ncl > waves) return 0;
-  if (env != 1 && (n_i * 100 < waves * IBC * 94 || j_count < (int64_t)PR_S * NB_PAIR_TJ)) return 0;
+  if (env != 1) {
+    // minimum fill of the wave's target slots, in 1/1000
+    static const int min_fill[8] = {1000, 1000, 865, 0, 0, 887, 900, 927};
+    if (n_i * 1000 < waves * ibc * min_fill[k] || j_count < (int64_t)PR_S * NB_PAIR_TJ) return 0;
+  }
+  if (k_out) *k_out = (int)k;
   return (int)ncl;
 }
 
@@ -2036,15 +2054,42 @@ static const void* pair_fn_of() {
   return reinterpret_cast<const void*>(&pair_kernel<Core, NB_PAIR_TJ>);
 }
 
-static cudaError_t launch_pair(StepArgs<float> a, int flags, int ncl, cudaStream_t stream) {
+struct PairFn {
+  const void* fn;
+  int64_t smem;
+};
+template <class Core>
+static PairFn pair_entry() {
+  return PairFn{pair_fn_of<Core>(), pair_smem_bytes<Core, NB_PAIR_TJ>()};
+}
+template <int K>
+static PairFn pair_entry_k(bool mask_self, bool uni) {
+  if constexpr (K < NB_PAIR_KMIN || K > NB_PAIR_K) {
+    return PairFn{nullptr, 0};
+  } else {
+    if (mask_self) return uni ? pair_entry<CorePair<K, true, true>>() : pair_entry<CorePair<K, true, false>>();
+    return uni ? pair_entry<CorePair<K, false, true>>() : pair_entry<CorePair<K, false, false>>();
+  }
+}
+static PairFn pair_entry_of(int k, bool mask_self, bool uni) {
+  switch (k) {
+    case 2: return pair_entry_k<2>(mask_self, uni);
+    case 3: return pair_entry_k<3>(mask_self, uni);
+    case 4: return pair_entry_k<4>(mask_self, uni);
+    case 5: return pair_entry_k<5>(mask_self, uni);
+    case 6: return pair_entry_k<6>(mask_self, uni);
+    case 7: return pair_entry_k<7>(mask_self, uni);
+    default: return PairFn{nullptr, 0};
+  }
+}
+
+static cudaError_t launch_pair(StepArgs<float> a, int flags, int ncl, int k, cudaStream_t stream) {
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
-  const void* fn = mask_self ? (uni ? pair_fn_of<CorePair<true, true>>() : pair_fn_of<CorePair<true, false>>())
-                             : (uni ? pair_fn_of<CorePair<false, true>>() : pair_fn_of<CorePair<false, false>>());
-  const int64_t smem = mask_self ? (uni ? pair_smem_bytes<CorePair<true, true>, NB_PAIR_TJ>()
-                                        : pair_smem_bytes<CorePair<true, false>, NB_PAIR_TJ>())
-                                 : (uni ? pair_smem_bytes<CorePair<false, true>, NB_PAIR_TJ>()
-                                        : pair_smem_bytes<CorePair<false, false>, NB_PAIR_TJ>());
+  const PairFn pf = pair_entry_of(k, mask_self, uni);
+  if (!pf.fn) return cudaErrorInvalidValue;
+  const void* fn = pf.fn;
+  const int64_t smem = pf.smem;
   {  // opt in to the dynamic shared memory once per (device, kernel)
     struct Opt { int dev; const void* fn; };
     static Opt opts[64];
@@ -2080,7 +2125,8 @@ static cudaError_t launch_pair(StepArgs<float> a, int flags, int ncl, cudaStream
 template <typename R>
 cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   if constexpr (sizeof(R) == 4) {
-    if (const int ncl = pair_clusters(a.n_i, a.j_count)) return launch_pair(a, flags, ncl, stream);
+    int k = 0;
+    if (const int ncl = pair_clusters(a.n_i, a.j_count, &k)) return launch_pair(a, flags, ncl, k, stream);
   }
   const StepGeometry g = step_geometry<R>(a.n_i, a.j_count);
   a.n_tiles = g.n_tiles;

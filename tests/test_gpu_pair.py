@@ -31,7 +31,11 @@ SCRIPT = textwrap.dedent(f"""
     cases = [("n1", 1, nb.uniform_cube, 1e-3), ("n33", 33, nb.uniform_cube, 1e-3),
              ("n4097", 4097, nb.uniform_cube, 1e-3), ("ragged_self", 12345, nb.uniform_cube, 0.0),
              ("uni", 15000, nb.plummer_sphere, 1e-4), ("c2", 16384, nb.uniform_cube, 1e-2),
-             ("full_wave", 16576, nb.uniform_cube, 1e-3)]
+             ("full_wave", 16576, nb.uniform_cube, 1e-3),
+             # the K family (2..7 targets per lane: 4736 ... 16576 target slots)
+             ("k2_full", 4736, nb.uniform_cube, 1e-3), ("k3", 7000, nb.uniform_cube, 1e-3),
+             ("k4_self_full", 9472, nb.uniform_cube, 0.0), ("k5", 11111, nb.uniform_cube, 1e-3),
+             ("k5_uni", 11000, nb.plummer_sphere, 1e-4), ("k6", 14000, nb.uniform_cube, 1e-2)]
     for name, n, gen, eps2 in cases:
         s = gen(n, 3, nb.Precision.SINGLE)
         pos = s.position_matrix().astype(np.float32)
@@ -87,7 +91,8 @@ def oracle():
     return O
 
 
-@pytest.mark.parametrize("name", ["n1", "n33", "n4097", "ragged_self", "uni", "c2", "full_wave"])
+@pytest.mark.parametrize("name", ["n1", "n33", "n4097", "ragged_self", "uni", "c2", "full_wave",
+                                  "k2_full", "k3", "k4_self_full", "k5", "k5_uni", "k6"])
 def test_forced_pair_kernel_vs_oracle(name, oracle, tmp_path):
     d = _run(tmp_path, 1)
     pos, eps2 = d[name + "_pos"], float(d[name + "_eps2"][0])
@@ -131,3 +136,18 @@ def test_pair_is_the_default_at_c2_and_stream_k_agrees(oracle, tmp_path):
     assert oracle.accel_dev(pair["c2"][rows], want) <= TOL_F32
     np.testing.assert_array_equal(auto["traj"], pair["traj"])
     assert oracle.position_dev(pair["traj"], sk["traj"]) <= 1e-5
+
+
+def test_k_family_selection():
+    """Which force kernel a launch shape takes (nb_dev_step_kernel): the cluster
+    kernel with the smallest K that holds the targets, where its slots are filled
+    to the measured break-even (DESIGN 3.4); stream-K elsewhere."""
+    from paper_2203_08263_b200 import _native
+    name = lambda n, j=None: _native.step_kernel_name(4, n, n if j is None else j)
+    for n in (4097, 4736, 5000, 7104, 8192, 9472, 10600, 11840, 12900, 14208, 15400, 16384, 16576):
+        assert name(n) == "pair_kernel", n
+    for n in (1000, 4096, 9600, 10000, 12000, 12700, 14500, 15300, 16577, 20000, 131072):
+        assert name(n) == "step_kernel", n
+    assert name(16384, 131072) == "pair_kernel"   # a rank's shard of C3 at 8 GPUs
+    assert name(8192, 1024) == "step_kernel"      # too few sources for 16 slices of one tile
+    assert _native.step_kernel_name(8, 8192, 8192) == "step_kernel"  # FP64 has no cluster kernel

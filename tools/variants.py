@@ -53,6 +53,10 @@ VARIANTS = {
     "pg1_infix": {"NB_PARTIAL_GROUPS": 1, "NB_INFIX_DEFAULT": 1},
     # round 2: the cluster split-source kernel with 6 targets per thread (no odd target)
     "pair_k6": {"NB_PAIR_K": 6},
+    "pair_k5": {"NB_PAIR_K": 5},
+    "pair_k4": {"NB_PAIR_K": 4},
+    "pair_k3": {"NB_PAIR_K": 3},
+    "pair_k2": {"NB_PAIR_K": 2},
     "pair_u8": {"NB_PAIR_UNROLL": 8},
     "pair_u12": {"NB_PAIR_UNROLL": 12},
     "pair_u32": {"NB_PAIR_UNROLL": 32},
