@@ -715,6 +715,13 @@ struct CoreF64 {
     for (int jj = 0; jj < TJ; ++jj) interact_g<NG>(tile_get<TJ>(tb, jj), jj);
 #endif
   }
+  // A full tile staged row-wise (packed 32-byte bodies, as a bulk copy leaves
+  // them: the cluster kernel's per-warp tiles).
+  template <int TJ>
+  __device__ __forceinline__ void full_tile_rows(const D4* tb) {
+#pragma unroll UNROLL_
+    for (int jj = 0; jj < TJ; ++jj) interact_g<KG>(tb[jj], jj);
+  }
   __device__ __forceinline__ void interact(const D4& pj, int jj) { interact_g<KG>(pj, jj); }
   // One source body against the first 2*NG targets (the rest are dead rows of a
   // partial i-block: skipped).
@@ -1441,6 +1448,153 @@ __global__ void __cluster_dims__(PR_CL, 1, 1) __launch_bounds__(PR_T, 1) pair_ke
   if (a.n_peers) __threadfence_system();
 }
 
+// ---------------------------------------------------------------- FP64 cluster split-source kernel
+// The same decomposition for FP64 (mid-size N in the reference's default
+// precision: the persistent stream-K kernel spends ~a third of a step at
+// N = 4096 on partial slots, the fixup pass and two grid barriers): 2-CTA
+// clusters, K = 2 or 4 targets per lane (4736 / 9472 target slots on 148 SMs),
+// 16 warp slices of the sources, each streamed by cp.async.bulk through the
+// warp's own double-buffered tiles of packed 32-byte bodies (read row-wise:
+// warp-wide broadcasts), slice sums reduced in fixed order through DSMEM.
+#ifndef NB_PAIR64_UNROLL
+#define NB_PAIR64_UNROLL 8
+#endif
+// minimum fill (1/1000) of the wave's target slots for K = 2 / K = 4 (1001 =
+// never): the measured break-even against the persistent / stream-K paths
+// (profiles/r02/pair_f64.txt) -- K = 2 wins from 2561 targets (above the small-N
+// kernel's range: +29 ... +44 % per launch), K = 4 from ~8150 (+3 % at 8192, +17 %
+// at 9472; below that its dead lanes cost more than the fixups it removes).
+#ifndef NB_PAIR64_FILL2
+#define NB_PAIR64_FILL2 540
+#endif
+#ifndef NB_PAIR64_FILL4
+#define NB_PAIR64_FILL4 860
+#endif
+template <int K, bool M, bool U> struct CorePair64 : CoreF64<K, M, NB_PAIR64_UNROLL, U> {
+  static constexpr bool MASK_SELF = M;
+};
+template <class Core, int TJ>
+constexpr int64_t pair64_smem_bytes() {
+  return (int64_t)PR_W * 2 * TJ * sizeof(D4) + (int64_t)3 * Core::K * PR_T * 8 + PR_W * 2 * 8;
+}
+
+template <class Core, int TJ>
+__global__ void __cluster_dims__(PR_CL, 1, 1) __launch_bounds__(PR_T, 1) pair_kernel_f64(const StepArgs<double> a) {
+  using B = D4;
+  constexpr int K = Core::K;
+  constexpr int IBC = 32 * K;
+  extern __shared__ __align__(128) unsigned char pr_smem[];
+  B* tiles = reinterpret_cast<B*>(pr_smem);                                 // [warp][2][TJ]
+  double* sums = reinterpret_cast<double*>(tiles + PR_W * 2 * TJ);          // [3K][PR_T]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sums + 3 * K * PR_T);        // [warp][2]
+  cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rank = (int)cluster.block_rank();
+  const int64_t blk = blockIdx.x / PR_CL;
+  const int64_t per = (a.j_count + PR_S * 16 - 1) / (PR_S * 16) * 16;
+  const int sl = rank * PR_W + warp;
+  const int64_t s0 = min(a.j_count, sl * per), s1 = min(a.j_count, s0 + per);
+  NB_DCHECK(blk * IBC < a.n_i && s0 >= 0 && s0 <= s1 && s1 <= a.j_count && rank < PR_CL);
+  B* tw = tiles + warp * 2 * TJ;
+  uint64_t* bw = bars + warp * 2;
+  if (lane == 0) {
+    mbar_init(bw, 1);
+    mbar_init(bw + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  NB_TRACE_ENTRY();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  NB_TRACE_WAITED();
+  asm volatile("griddepcontrol.launch_dependents;");
+
+  Core core;
+  core.init(a.eps2, nullptr, 0);
+#pragma unroll
+  for (int q = 0; q < K / 2; ++q) {
+    const int64_t i0 = blk * IBC + (2 * q) * 32 + lane, i1 = i0 + 32;
+    core.set_pair(q, ld4(a.pos + a.i_begin + (i0 < a.n_i ? i0 : a.n_i - 1)),
+                  ld4(a.pos + a.i_begin + (i1 < a.n_i ? i1 : a.n_i - 1)));
+  }
+  core.zero_sums();
+
+  auto issue = [&](int buf, int64_t lo) {
+    if (lane == 0) {
+      const int64_t cnt = min((int64_t)TJ, s1 - lo);
+      int64_t jg = a.j_begin + lo;
+      if (jg >= a.n_all) jg -= a.n_all;
+      const int64_t n1 = min(cnt, a.n_all - jg);
+      NB_DCHECK(cnt > 0 && cnt <= TJ && jg >= 0 && jg + n1 <= a.n_all && cnt - n1 <= a.n_all);
+      mbar_expect_tx(bw + buf, (uint32_t)(cnt * sizeof(B)));
+      bulk_g2s(tw + buf * TJ, a.pos + jg, (uint32_t)(n1 * sizeof(B)), bw + buf);
+      if (cnt > n1) bulk_g2s(tw + buf * TJ + n1, a.pos, (uint32_t)((cnt - n1) * sizeof(B)), bw + buf);
+    }
+  };
+  uint32_t phase_bits = 0u;
+  if (s0 < s1) issue(0, s0);
+  int buf = 0;
+  for (int64_t lo = s0; lo < s1; lo += TJ) {
+    const bool more = lo + TJ < s1;
+    mbar_wait(bw + buf, (phase_bits >> buf) & 1u);
+    phase_bits ^= 1u << buf;
+    if (more) issue(buf ^ 1, lo + TJ);  // buf^1 was released by the __syncwarp below
+    const B* tb = tw + buf * TJ;
+    const int count = (int)min((int64_t)TJ, s1 - lo);
+    if (Core::MASK_SELF) {
+      int64_t base = a.j_begin + lo;
+      if (base >= a.n_all) base -= a.n_all;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        int64_t rel = a.i_begin + blk * IBC + k * 32 + lane - base;
+        if (rel < 0) rel += a.n_all;
+        core.selfj[k] = rel < count ? (int)rel : -1;
+      }
+    }
+    if (count == TJ) {
+      core.template full_tile_rows<TJ>(tb);
+    } else {
+      int jj = 0;
+#pragma unroll 1
+      for (; jj + 4 <= count; jj += 4) {
+        core.interact(tb[jj], jj);
+        core.interact(tb[jj + 1], jj + 1);
+        core.interact(tb[jj + 2], jj + 2);
+        core.interact(tb[jj + 3], jj + 3);
+      }
+#pragma unroll 1
+      for (; jj < count; ++jj) core.interact(tb[jj], jj);
+    }
+    buf ^= 1;
+    __syncwarp();
+  }
+  // this thread's slice sums (registers) into the CTA's shared block
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sums[(d * K + k) * PR_T + tid] = core.sum(d, k);
+
+  cluster.sync();  // every slice's sums visible to both CTAs
+  const double* part[PR_CL];
+#pragma unroll
+  for (int r = 0; r < PR_CL; ++r) part[r] = cluster.map_shared_rank(sums, r);
+  for (int t = rank * (IBC / 2) + tid; t < (rank + 1) * (IBC / 2); t += PR_T) {
+    const int k = t >> 5, l = t & 31;
+    NB_DCHECK(k < K && t < IBC);
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int s = 0; s < PR_S; ++s) {
+      const double* q = part[s / PR_W] + (s % PR_W) * 32 + l;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) acc[d] += q[(d * K + k) * PR_T];
+    }
+    const int64_t il = blk * IBC + t;
+    if (il < a.n_i) finalize_body<double>(a, il, acc[0], acc[1], acc[2]);
+  }
+  cluster.sync();  // the peer's sums stay alive until both CTAs have read them
+  NB_TRACE_END(5);
+  if (a.n_peers) __threadfence_system();
+}
+
 // ---------------------------------------------------------------- split i-block fixup
 template <typename R, int IB>
 __device__ __forceinline__ void fixup_body(const StepArgs<R>& a, int64_t il);
@@ -2083,10 +2237,57 @@ static PairFn pair_entry_of(int k, bool mask_self, bool uni) {
   }
 }
 
+template <typename R>
+static cudaError_t launch_pair_fn(StepArgs<R>& a, const PairFn& pf, int ncl, cudaStream_t stream);
+
 static cudaError_t launch_pair(StepArgs<float> a, int flags, int ncl, int k, cudaStream_t stream) {
   const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
   a.uniform_mass = uni ? 1 : 0;
-  const PairFn pf = pair_entry_of(k, mask_self, uni);
+  return launch_pair_fn<float>(a, pair_entry_of(k, mask_self, uni), ncl, stream);
+}
+
+// FP64: K = 2 (up to 4736 targets on 148 SMs) or 4 (9472), taken where measured
+// faster than the persistent / stream-K paths (profiles/r02/pair_f64.txt).
+static int pair64_clusters(int64_t n_i, int64_t j_count, int* k_out = nullptr) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("NB_PAIR");
+    env = e ? atoi(e) : -1;
+  }
+  if (env == 0 || n_i < 1) return 0;
+  const int64_t waves = sm_count() / PR_CL;
+  const int64_t need = (n_i + waves * 32 - 1) / (waves * 32);
+  const int64_t k = need <= 2 ? 2 : 4;
+  if (need > 4) return 0;
+  const int64_t ibc = 32 * k;
+  const int64_t ncl = (n_i + ibc - 1) / ibc;
+  if (ncl > waves) return 0;
+  if (env != 1) {
+    static const int min_fill[5] = {1000, 1000, NB_PAIR64_FILL2, 1000, NB_PAIR64_FILL4};  // 1/1000 of the slots
+    // (>= 128 sources per warp slice: measured faster from 2561 sources on, partial tiles included)
+    if (n_i * 1000 < waves * ibc * min_fill[k] || j_count < (int64_t)PR_S * NB_PAIR_TJ / 2) return 0;
+  }
+  if (k_out) *k_out = (int)k;
+  return (int)ncl;
+}
+template <class Core>
+static PairFn pair64_entry() {
+  return PairFn{reinterpret_cast<const void*>(&pair_kernel_f64<Core, NB_PAIR_TJ>), pair64_smem_bytes<Core, NB_PAIR_TJ>()};
+}
+template <int K>
+static PairFn pair64_entry_k(bool mask_self, bool uni) {
+  if (mask_self) return uni ? pair64_entry<CorePair64<K, true, true>>() : pair64_entry<CorePair64<K, true, false>>();
+  return uni ? pair64_entry<CorePair64<K, false, true>>() : pair64_entry<CorePair64<K, false, false>>();
+}
+static cudaError_t launch_pair64(StepArgs<double> a, int flags, int ncl, int k, cudaStream_t stream) {
+  const bool mask_self = (flags & 1) != 0, uni = (flags & 2) != 0;
+  a.uniform_mass = uni ? 1 : 0;
+  return launch_pair_fn<double>(a, k == 2 ? pair64_entry_k<2>(mask_self, uni) : pair64_entry_k<4>(mask_self, uni), ncl,
+                                stream);
+}
+
+template <typename R>
+static cudaError_t launch_pair_fn(StepArgs<R>& a, const PairFn& pf, int ncl, cudaStream_t stream) {
   if (!pf.fn) return cudaErrorInvalidValue;
   const void* fn = pf.fn;
   const int64_t smem = pf.smem;
@@ -2127,6 +2328,9 @@ cudaError_t launch_step(StepArgs<R> a, int flags, cudaStream_t stream) {
   if constexpr (sizeof(R) == 4) {
     int k = 0;
     if (const int ncl = pair_clusters(a.n_i, a.j_count, &k)) return launch_pair(a, flags, ncl, k, stream);
+  } else {
+    int k = 0;
+    if (const int ncl = pair64_clusters(a.n_i, a.j_count, &k)) return launch_pair64(a, flags, ncl, k, stream);
   }
   const StepGeometry g = step_geometry<R>(a.n_i, a.j_count);
   a.n_tiles = g.n_tiles;
@@ -2182,6 +2386,8 @@ template <typename R>
 const char* step_kernel_name(int64_t n_i, int64_t j_count) {
   if constexpr (sizeof(R) == 4) {
     if (pair_clusters(n_i, j_count)) return "pair_kernel";
+  } else {
+    if (pair64_clusters(n_i, j_count)) return "pair_kernel";
   }
   return "step_kernel";
 }

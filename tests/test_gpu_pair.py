@@ -150,4 +150,40 @@ def test_k_family_selection():
         assert name(n) == "step_kernel", n
     assert name(16384, 131072) == "pair_kernel"   # a rank's shard of C3 at 8 GPUs
     assert name(8192, 1024) == "step_kernel"      # too few sources for 16 slices of one tile
-    assert _native.step_kernel_name(8, 8192, 8192) == "step_kernel"  # FP64 has no cluster kernel
+    # FP64 (pair_kernel_f64, K = 2 / 4): above the small-N kernel's range up to 4736, and 8146 ... 9472
+    name64 = lambda n, j=None: _native.step_kernel_name(8, n, n if j is None else j)
+    for n in (2561, 3072, 4096, 4736, 8192, 9000, 9472):
+        assert name64(n) == "pair_kernel", n
+    for n in (1024, 2557, 4737, 6144, 8000, 9473, 16384, 131072):
+        assert name64(n) == "step_kernel", n
+    assert name64(4096, 524288) == "pair_kernel" and name64(4096, 2047) == "step_kernel"
+
+
+@pytest.mark.parametrize("n,eps2,gen", [(2561, 1e-3, "uniform_cube"), (4096, 1e-3, "uniform_cube"),
+                                        (4736, 0.0, "uniform_cube"), (3000, 1e-4, "plummer_sphere"),
+                                        (8192, 1e-2, "uniform_cube"), (9472, 0.0, "uniform_cube")])
+def test_fp64_cluster_kernel_vs_oracle(n, eps2, gen, oracle):
+    """pair_kernel_f64 (the default at these sizes): accelerations against the
+    long-double oracle at the north star's FP64 bound, bitwise run to run, and a
+    4-step trajectory through simulate() (per-step launches of the cluster kernel)."""
+    import paper_2203_08263_b200 as nb
+    from paper_2203_08263_b200 import _native
+    from paper_2203_08263_b200.device import DeviceState, kernel_flags
+    assert _native.step_kernel_name(8, n, n) == "pair_kernel"
+    s = getattr(nb, gen)(n, 3, nb.Precision.DOUBLE)
+    pos = s.position_matrix()
+    st = DeviceState(pos, np.stack(s.velocities, 1), s.masses, np.float64)
+    f = kernel_flags(s.masses, eps2, np.float64)
+    a = st.accelerations(1.0, eps2, f)[:, :3].cpu().numpy()
+    b = st.accelerations(1.0, eps2, f)[:, :3].cpu().numpy()
+    np.testing.assert_array_equal(a, b)
+    rows = _rows(n)
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)), s.masses, rows, 1.0, eps2)
+    dev = oracle.accel_dev(a[rows], want)
+    print(n, "accel_dev", dev)
+    assert dev <= 1e-12
+    p = nb.SimParams(1.0, 1e-4, eps2, 4)
+    fin = nb.simulate(s, p).position_matrix()
+    ref, _ = oracle.simulate(pos, np.stack(s.velocities, 1), s.masses, 1.0, p.dt, eps2, 4,
+                             threads=oracle.host_threads())
+    assert oracle.position_dev(fin, ref) <= 1e-12

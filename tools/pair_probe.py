@@ -12,15 +12,18 @@ from paper_2203_08263_b200.device import DeviceState, kernel_flags
 from paper_2203_08263_b200._native import NB_MODE_ACCEL
 
 CLK = 1.965e9
+PREC = nb.Precision(os.environ.get("NB_PROBE_PREC", "single"))  # NB_PROBE_PREC=double: the FP64 kernels
+DT = PREC.dtype
+LANES = 256 if PREC is nb.Precision.SINGLE else 128
 js = []
 if "--j" in sys.argv:
     k = sys.argv.index("--j")
     js = [int(v) for v in sys.argv[k + 1].split(",")]
     del sys.argv[k:k + 2]
 for n in [int(a) for a in sys.argv[1:]]:
-    s = nb.uniform_cube(n, 0, nb.Precision.SINGLE)
-    st = DeviceState(s.position_matrix().astype(np.float32), np.stack(s.velocities, 1), s.masses, np.float32)
-    flags = kernel_flags(s.masses, 1e-3, np.float32)
+    s = nb.uniform_cube(n, 0, PREC)
+    st = DeviceState(s.position_matrix().astype(DT), np.stack(s.velocities, 1), s.masses, DT)
+    flags = kernel_flags(s.masses, 1e-3, DT)
     reps = max(10, int(2e11 / (n * n)))
     for _ in range(3):
         st.step(1.0, 1e-3, 0.0, NB_MODE_ACCEL, flags)
@@ -36,7 +39,7 @@ for n in [int(a) for a in sys.argv[1:]]:
         best = min(best, e0.elapsed_time(e1) / 1e3 / reps)
     inter = float(n) * n
     print(json.dumps({"n": n, "pair": os.environ.get("NB_PAIR", "auto"), "us": best * 1e6,
-                      "frac_nominal": 20 * inter / best / (148 * 256 * CLK),
+                      "frac_nominal": 20 * inter / best / (148 * LANES * CLK),
                       "int_per_clk_sm": inter / best / CLK / 148}), flush=True)
     for j in js:
         def run():
