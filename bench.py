@@ -492,7 +492,7 @@ def run_ours(args) -> dict:
         # that kernel; its steps+1 force evaluations are the algorithmic work.
         mean_launch_s = statistics.mean(step_ms) / 1e3
         achieved = FLOP_PER_INTERACTION * float(cfg.n) * cfg.n * (steps + 1) / mean_launch_s / 1e12
-        kernel_name = ("nb::small_simulate_kernel" if cfg.n <= (4096 if pbytes == 4 else 2560)
+        kernel_name = ("nb::small_simulate_kernel" if cfg.n <= (3584 if pbytes == 4 else 2560)
                        else "nb::simulate_kernel") + " (the whole simulate in one cooperative launch)"
         launch_timing = "CUDA events around each timed step = around its single launch"
     elif world == 1:

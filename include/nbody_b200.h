@@ -196,7 +196,7 @@ int nb_dev_step_p2p_f64(const void* pos4, int64_t n_all, int64_t i_begin, int64_
  * evaluation and kick (steps+1 force evaluations), ping-ponging pos4_a <-> pos4_b.
  * On return (stream-ordered) the final positions are in pos4_a if steps is even,
  * else in pos4_b; *final_in_b reports which (may be NULL).  Small N runs the whole
- * loop in one cooperative launch: N <= 4096 (FP32) / 2560 (FP64) with the source
+ * loop in one cooperative launch: N <= 3584 (FP32) / 2560 (FP64) with the source
  * split inside each CTA (environment NB_SMALL_MAX_N overrides, 0 disables; its
  * summation order differs from the per-step path, results agree within the
  * parity tolerances), up to 8192 with the per-step decomposition (bitwise equal

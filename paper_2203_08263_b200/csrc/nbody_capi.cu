@@ -54,7 +54,7 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 #ifndef NB_SMALL_MAX_N_F32
-#define NB_SMALL_MAX_N_F32 4096
+#define NB_SMALL_MAX_N_F32 3584
 #endif
 #ifndef NB_SMALL_MAX_N_F64
 #define NB_SMALL_MAX_N_F64 2560

@@ -30,7 +30,7 @@
 //    order -- bitwise reproducible run to run -- which then runs the epilogue.
 //  * NB_TRACE builds record per-CTA %globaltimer timelines (tools/trace_launches.py).
 //  * Small N: the whole multi-step loop runs in one cooperative launch --
-//    small_simulate_kernel (N <= 4096 FP32 / 2560 FP64: source split inside the
+//    small_simulate_kernel (N <= 3584 FP32 / 2560 FP64: source split inside the
 //    CTA, no global partials; between its first and last step the positions are
 //    exchanged as tagged coherent records, the staging poll standing in for the
 //    grid barrier) or simulate_kernel (up to 8192: the stream-K decomposition
@@ -2176,7 +2176,9 @@ static int sm_count() {
 // targets per lane K: the smallest K whose one wave of 2-CTA clusters (74 * 32 * K
 // target slots on 148 SMs) holds the launch's targets, taken when the slots are
 // filled at least to the measured break-even against the stream-K / persistent
-// paths (profiles/r02/pair_kfam.txt: K <= 4 wins over its whole range, K = 5, 6,
+// paths (profiles/r02/pair_kfam.txt: K = 2 from 3585 targets -- a 10-step simulate
+// at N = 4096 takes 13.1 us per evaluation against the small-N kernel's 15.0, the
+// crossover is ~3600 --, K = 3, 4 over their whole range, K = 5, 6,
 // 7 from 88.7 / 90 / 92.7 %: K = 7 from 15367 targets, where stream-K needs its 11th i-block) and every warp's source slice holds at least one
 // full tile.  NB_PAIR=0 / 1 turns it off / on wherever the targets fit one wave
 // (A/B measurements, tests).
@@ -2196,8 +2198,9 @@ static int pair_clusters(int64_t n_i, int64_t j_count, int* k_out = nullptr) {
   if (ncl > waves) return 0;
   if (env != 1) {
     // minimum fill of the wave's target slots, in 1/1000
-    static const int min_fill[8] = {1000, 1000, 865, 0, 0, 887, 900, 927};
-    if (n_i * 1000 < waves * ibc * min_fill[k] || j_count < (int64_t)PR_S * NB_PAIR_TJ) return 0;
+    static const int min_fill[8] = {1000, 1000, 757, 0, 0, 887, 900, 927};
+    // (>= 128 sources per warp slice: partial tiles included, still ahead of the other paths)
+    if (n_i * 1000 < waves * ibc * min_fill[k] || j_count < (int64_t)PR_S * NB_PAIR_TJ / 2) return 0;
   }
   if (k_out) *k_out = (int)k;
   return (int)ncl;

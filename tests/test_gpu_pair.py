@@ -144,9 +144,9 @@ def test_k_family_selection():
     to the measured break-even (DESIGN 3.4); stream-K elsewhere."""
     from paper_2203_08263_b200 import _native
     name = lambda n, j=None: _native.step_kernel_name(4, n, n if j is None else j)
-    for n in (4097, 4736, 5000, 7104, 8192, 9472, 10600, 11840, 12900, 14208, 15400, 16384, 16576):
+    for n in (3600, 4096, 4097, 4736, 5000, 7104, 8192, 9472, 10600, 11840, 12900, 14208, 15400, 16384, 16576):
         assert name(n) == "pair_kernel", n
-    for n in (1000, 4096, 9600, 10000, 12000, 12700, 14500, 15300, 16577, 20000, 131072):
+    for n in (1000, 3500, 9600, 10000, 12000, 12700, 14500, 15300, 16577, 20000, 131072):
         assert name(n) == "step_kernel", n
     assert name(16384, 131072) == "pair_kernel"   # a rank's shard of C3 at 8 GPUs
     assert name(8192, 1024) == "step_kernel"      # too few sources for 16 slices of one tile

@@ -451,7 +451,7 @@ def test_exchange_c_abi_single_gpu():
 @pytest.mark.parametrize("n", [2560, 2561, 4096, 4097, 8192, 8193])
 def test_simulate_path_boundaries(prec, n, oracle):
     """simulate() switches kernels with N (small-N cooperative kernel up to
-    4096 FP32 / 2560 FP64, stream-K persistent kernel up to 8192, per-step
+    3584 FP32 / 2560 FP64, cluster kernels or the stream-K persistent kernel up to 8192, per-step
     launches beyond): trajectories on both sides of each switch agree with the
     FP64 oracle."""
     s = cube(n, 11, prec)
