@@ -187,3 +187,27 @@ def test_fp64_cluster_kernel_vs_oracle(n, eps2, gen, oracle):
     ref, _ = oracle.simulate(pos, np.stack(s.velocities, 1), s.masses, 1.0, p.dt, eps2, 4,
                              threads=oracle.host_threads())
     assert oracle.position_dev(fin, ref) <= 1e-12
+
+
+def test_fp64_cluster_kernel_sharded_carry_vs_oracle(oracle):
+    """One rank of a 3-way FP64 shard (rows [3000, 6000) of 9000) through
+    pair_kernel_f64: its own sources into the FP64 carry, then the circular
+    remainder (run_sharded's two phases), against the long-double oracle."""
+    import paper_2203_08263_b200 as nb
+    from paper_2203_08263_b200 import _native
+    from paper_2203_08263_b200._native import NB_MODE_ACCEL
+    from paper_2203_08263_b200.device import DeviceState, kernel_flags
+    n, i0, ni = 9000, 3000, 3000
+    assert _native.step_kernel_name(8, ni, ni) == "pair_kernel" and _native.step_kernel_name(8, ni, n - ni) == "pair_kernel"
+    s = nb.uniform_cube(n, 4, nb.Precision.DOUBLE)
+    pos = s.position_matrix()
+    st = DeviceState(pos, np.stack(s.velocities, 1), s.masses, np.float64, i_begin=i0, n_i=ni)
+    f = kernel_flags(s.masses, 1e-3, np.float64)
+    st.step(1.0, 1e-3, 0.0, NB_MODE_ACCEL, f, j_begin=i0, j_count=ni, carry_mode=1)
+    st.step(1.0, 1e-3, 0.0, NB_MODE_ACCEL, f, j_begin=i0 + ni, j_count=n - ni, carry_mode=2)
+    got = st.acc[:ni, :3].cpu().numpy()
+    local = _rows(ni)
+    want = oracle.accel_rows_ld(*(np.ascontiguousarray(pos[:, k]) for k in range(3)), s.masses, i0 + local, 1.0, 1e-3)
+    dev = oracle.accel_dev(got[local], want)
+    print("fp64 shard accel_dev", dev)
+    assert dev <= 1e-12
